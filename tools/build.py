@@ -1,0 +1,131 @@
+#!/usr/bin/env python3
+"""Build every native artefact in-tree (the .so files travel to the GPU box).
+
+Targets:
+  oracle       oracle/liboracle.so            gcc, -O2 -ffp-contract=off -fno-fast-math (CPU oracle)
+  inputs       inputs/libmoa_inputs.so         gcc (host input generator)
+  inputs_cuda  inputs/libmoa_inputs_cuda.so    nvcc sm_100a (device input generator)
+  moa          paper_2306_11148_b200/libmoa.so nvcc sm_100a (the product: C-ABI + kernels, links NCCL)
+  all          everything (default)
+
+Incremental: a target is rebuilt only when a source/header is newer than its output
+(or with --force). The oracle and the product share no sources, headers or flags.
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_root() -> str:
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    cands = []
+    if spec and spec.submodule_search_locations:
+        for loc in spec.submodule_search_locations:
+            cands.append(os.path.join(loc, "nccl"))
+    cands.append("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl")
+    for c in cands:
+        if os.path.exists(os.path.join(c, "include", "nccl.h")):
+            return c
+    raise RuntimeError("NCCL headers not found (torch-bundled nvidia/nccl expected)")
+
+
+def _stale(out: str, deps: list[str]) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str]):
+    print("  $", " ".join(cmd), flush=True)
+    subprocess.check_call(cmd, cwd=ROOT)
+
+
+def build_oracle(force=False):
+    src = os.path.join(ROOT, "oracle", "moa_oracle.c")
+    out = os.path.join(ROOT, "oracle", "liboracle.so")
+    if force or _stale(out, [src]):
+        _run(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-shared", "-pthread",
+              src, "-o", out, "-lm"])
+    return out
+
+
+def build_inputs(force=False):
+    src = os.path.join(ROOT, "inputs", "moa_inputs.c")
+    hdr = os.path.join(ROOT, "inputs", "moa_inputs.h")
+    out = os.path.join(ROOT, "inputs", "libmoa_inputs.so")
+    if force or _stale(out, [src, hdr]):
+        _run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", src, "-o", out])
+    return out
+
+
+def build_inputs_cuda(force=False):
+    src = os.path.join(ROOT, "inputs", "moa_inputs_cuda.cu")
+    hdr = os.path.join(ROOT, "inputs", "moa_inputs.h")
+    out = os.path.join(ROOT, "inputs", "libmoa_inputs_cuda.so")
+    if force or _stale(out, [src, hdr]):
+        _run([NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", src, "-o", out])
+    return out
+
+
+def build_moa(force=False, verbose_ptxas=False):
+    pkg = os.path.join(ROOT, "paper_2306_11148_b200")
+    csrc = os.path.join(pkg, "csrc")
+    srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cpp")))
+    hdrs = sorted(glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh"))
+                  + glob.glob(os.path.join(ROOT, "include", "*.h")))
+    out = os.path.join(pkg, "libmoa.so")
+    nccl = _nccl_root()
+    objdir = os.path.join(ROOT, "build", "moa")
+    os.makedirs(objdir, exist_ok=True)
+    if not (force or _stale(out, srcs + hdrs)):
+        return out
+    common = [*ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+              "-I", csrc, "-I", os.path.join(nccl, "include")]
+    if verbose_ptxas:
+        common += ["-Xptxas", "-v"]
+    objs = []
+    jobs = []
+    for s in srcs:
+        o = os.path.join(objdir, os.path.basename(s) + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + hdrs):
+            jobs.append([NVCC, *common, "-c", s, "-o", o])
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        for f in [ex.submit(_run, j) for j in jobs]:
+            f.result()
+    _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+          "-Xlinker", "-rpath=" + os.path.join(nccl, "lib"), "-lcudart"])
+    return out
+
+
+TARGETS = {"oracle": build_oracle, "inputs": build_inputs, "inputs_cuda": build_inputs_cuda, "moa": build_moa}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("targets", nargs="*", default=["all"])
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--ptxas-v", action="store_true")
+    a = ap.parse_args(argv)
+    names = list(TARGETS) if "all" in a.targets else a.targets
+    for n in names:
+        print(f"[build] {n}", flush=True)
+        if n == "moa":
+            build_moa(a.force, a.ptxas_v)
+        else:
+            TARGETS[n](a.force)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
