@@ -1,0 +1,183 @@
+/* moa.h — C ABI of the B200-native MoA Operational-Normal-Form GEMM (libmoa.so).
+ *
+ * Paper: L. Mullin et al., "From array algebra to energy efficiency on GPUs"
+ * (arXiv 2306.11148); "P:n" = line n of PAPER.md. Design: DESIGN.md.
+ *
+ * Everything here is plain C: integers, raw pointers, opaque handles. No torch
+ * types. All matrices are ROW-MAJOR and CONTIGUOUS ("generic row-major form",
+ * P:77-82; "ALL arrays are accessed contiguously"):
+ *     A<m,n>: element (i,k) at A[(i*n)+k];  B<n,p>: (k,j) at B[(k*p)+j];
+ *     C<m,p>: (i,j) at C[(i*p)+j]            (Eq. 1; Eq. 3)
+ *
+ * Ownership: the caller owns every buffer. The library never allocates device
+ * memory per call, never frees caller memory and never synchronises the
+ * caller's stream (except moa_gemm_host, which is documented as synchronous).
+ * The library owns only communicator handles (moa_comm_t) and a mutex-guarded
+ * per-device cache of device properties.
+ *
+ * Errors: every entry point returns a moa_status. Argument validation happens
+ * before any CUDA or NCCL call, so an invalid call has no side effect. CUDA
+ * launch errors map to MOA_ERR_CUDA and NCCL errors to MOA_ERR_NCCL, with detail
+ * in moa_last_error() (thread-local). Asynchronous device faults surface at the
+ * caller's next synchronisation, as in CUDA. Nothing aborts or prints.
+ */
+#ifndef MOA_H
+#define MOA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOA_ABI_VERSION 1
+
+/* Element types. MOA_F64 is the paper's type (double).
+ * MOA_F32: exact fp32, one IEEE fma per (i,j,k), k ascending.
+ * MOA_F32_3XTF32: fp32 in/out via three TF32 tensor-core products
+ *   (big*big + big*small + small*big); NOT exact, tolerance 5e-3 (north_star). */
+typedef enum { MOA_F64 = 0, MOA_F32 = 1, MOA_F32_3XTF32 = 2 } moa_dtype;
+
+typedef enum {
+  MOA_OK = 0,
+  MOA_ERR_INVALID_SHAPE = 1,   /* negative extent, overflow of m*n / n*p / m*p, bad partition */
+  MOA_ERR_INVALID_DTYPE = 2,
+  MOA_ERR_NULL_POINTER = 3,    /* NULL where the extents require memory */
+  MOA_ERR_ALIASING = 4,        /* C overlaps A or B (":=" needs distinct output) */
+  MOA_ERR_MISALIGNED = 5,      /* pointer not aligned to the element size */
+  MOA_ERR_INVALID_INDEX = 6,   /* psi index out of bounds (0 <=* i <* rho xi) */
+  MOA_ERR_CUDA = 7,
+  MOA_ERR_NCCL = 8,
+  MOA_ERR_UNSUPPORTED_DEVICE = 9 /* not an sm_100 device */
+} moa_status;
+
+/* Kernels the static plan can choose. */
+typedef enum {
+  MOA_KERNEL_NONE = 0,          /* no work (m == 0 or p == 0) */
+  MOA_KERNEL_ZERO_FILL = 1,     /* n == 0: C := 0 (empty sum) */
+  MOA_KERNEL_DGEMM_TMA = 2,     /* K1: fp64 DMMA, TMA + mbarrier warp-specialised */
+  MOA_KERNEL_DGEMM_GENERIC = 3, /* K2: fp64 DMMA, plain loads (odd n/p, unaligned) */
+  MOA_KERNEL_SGEMM_FFMA = 4,    /* K3: exact fp32 FFMA */
+  MOA_KERNEL_SGEMM_3XTF32 = 5   /* K4: 3xTF32 on tcgen05 tensor cores */
+} moa_kernel;
+
+/* Static block plan ("block sizes derived statically from shapes and types",
+ * P:12-13; "make [sizel, sizer] as close as possible to the GPU cache sizes",
+ * P:238-245). Pure function of (m, n, p, dtype, device properties); no
+ * autotuning. bk and the k order depend only on dtype, never on m, so any row
+ * block computed alone is bitwise equal to the same rows of the full product. */
+typedef struct {
+  int32_t kernel;        /* moa_kernel */
+  int32_t bm, bn, bk;    /* CTA tile: the lifted block of C (bm x bn) and k-slab bk */
+  int32_t stages;        /* shared-memory ring depth */
+  int32_t threads;       /* threads per CTA */
+  int32_t ctas_per_sm;   /* resident CTAs per SM the plan assumes */
+  int32_t grid;          /* CTAs launched (persistent: min(tiles, sms*ctas_per_sm)) */
+  int64_t tiles_m, tiles_n, tiles; /* ceil(m/bm), ceil(p/bn), product */
+  int32_t raster_group;  /* tile-rows per rasterisation group (L2 reuse) */
+  int32_t smem_bytes;    /* dynamic shared memory per CTA */
+  int32_t sms;           /* SM count of the device planned for */
+  int32_t reserved;
+} moa_plan_t;
+
+/* Opaque NCCL-backed communicator owned by the library. */
+typedef struct moa_comm_s* moa_comm_t;
+
+/* ------------------------------------------------------------------------
+ * moa_gemm — C := A • B  (Eq. 3 / Eq. 5), ONF row-major contiguous.
+ *   m, n, p : extents, >= 0 (rho A = <m,n>, rho B = <n,p>, rho C = <m,p>).
+ *   A, B, C : DEVICE pointers of element type `dtype` (moa_dtype), row-major
+ *             contiguous as above. C is overwritten (":=", reading R1); its
+ *             byte range must not overlap A's or B's (MOA_ERR_ALIASING).
+ *             Pointers must be aligned to the element size; 16-byte alignment
+ *             with n, p even (f64) / multiples of 4 (f32) selects the TMA kernel,
+ *             anything else the generic kernel (same results, bit for bit).
+ *   stream  : cudaStream_t as void* (NULL = legacy default stream). Asynchronous.
+ * m == 0 or p == 0: no-op. n == 0: C := 0 (cudaMemsetAsync).
+ * Result (f64, f32): for every (i,j), the fma chain over k = 0..n-1 ascending
+ * starting from +0 — i.e. Fig. 3 ip.c with its update contracted to
+ * one fused multiply-add (reading R3), bitwise, for any finite inputs.
+ * ------------------------------------------------------------------------ */
+int moa_gemm(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype, void* stream);
+
+/* moa_gemm with an explicit plan (from moa_plan, possibly edited: only bm/bn/
+ * stages/raster_group/grid of a kernel-compatible plan are honoured). Used by the
+ * block-size sweep (the paper's block-size experiment). Returns
+ * MOA_ERR_INVALID_SHAPE if the plan is not valid for the shape/dtype. */
+int moa_gemm_with_plan(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype,
+                       const moa_plan_t* plan, void* stream);
+
+/* moa_gemm_host — end-to-end call on HOST buffers: copies A_host and B_host into
+ * the caller's device buffers A_dev/B_dev (cudaMemcpyAsync H2D), runs moa_gemm
+ * into C_dev, copies C_dev back to C_host (D2H), then synchronises `stream`.
+ * Host buffers should be pinned for asynchronous copies. Same validation as
+ * moa_gemm on the device buffers; host pointers must be non-NULL when their
+ * extents are non-zero. */
+int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
+                  void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream);
+
+/* ------------------------------------------------------------------------
+ * moa_gemm_lifted — row-lifted C := A • B over the communicator's G ranks
+ * (dimension lifting of the i loop onto processors, Fig. 4
+ * ip_rows.c P:150-171). COLLECTIVE: every rank calls it with identical m, n, p,
+ * dtype. Rank g owns rows [row0_g, row0_g + rows_g) of A and C, with
+ * (row0_g, rows_g) = moa_lift_rows(m, G, g).
+ *   A_local : device, rows_g x n (rank g's rows of A).
+ *   B       : device, n x p on every rank; input on rank 0, overwritten with
+ *             rank 0's B on the others (in-place ncclBroadcast over NVLink —
+ *             every processor needs all of B: B carries no processor index in
+ *             ip_rows.c; reading R13).
+ *   C_local : device, rows_g x p, receives rank g's rows of C.
+ *   C_full  : NULL, or a device m x p buffer that receives all of C on every
+ *             rank (gather, reading R14).
+ * Bitwise identical to moa_gemm on one GPU (row-block invariance of the plan).
+ * Errors are detected identically on every rank before any NCCL call.
+ * ------------------------------------------------------------------------ */
+int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
+                    int dtype, void* stream, moa_comm_t comm);
+
+/* ------------------------------------------------------------------------
+ * moa_psi — MoA psi on a row-major array (appendix; bracket bridge
+ * rav(i psi xi) == (rav xi)[gamma(i; rho xi)]):
+ *   rank, shape[0..rank): rho xi (extents >= 0). rank == 0 is a scalar.
+ *   q, idx[0..q): a full (q == rank) or prefix (q < rank) index, 0 <= idx[d] < shape[d].
+ *   out: *offset = gamma_row(idx ++ 0...; shape), *count = prod(shape[q..rank)).
+ *   psi(idx, xi) is the CONTIGUOUS slice rav(xi)[*offset, *offset + *count).
+ * Errors: MOA_ERR_INVALID_INDEX (q > rank, or an index out of bounds),
+ * MOA_ERR_INVALID_SHAPE (negative extent or overflow), MOA_ERR_NULL_POINTER.
+ * In the ONF, psi(<i>, A) = [i*n, i*n+n) and psi(<sigma>, B) = [sigma*p, sigma*p+p):
+ * the contiguous rows of Fig. 1.
+ * ------------------------------------------------------------------------ */
+int moa_psi(int rank, const int64_t* shape, int q, const int64_t* idx, int64_t* offset, int64_t* count);
+
+/* moa_lift_rows — dimension lifting of the row axis: part `part` of `nparts`
+ * (P:142-148). Balanced contiguous split (reading R5; ip_rows.c's sizel/np
+ * would drop m mod np rows): rows = floor(m/G) + (g < m mod G),
+ * row0 = g*floor(m/G) + min(g, m mod G). Equals the listing's split when G | m.
+ * Errors: MOA_ERR_INVALID_SHAPE (m < 0, nparts <= 0, part out of range). */
+int moa_lift_rows(int64_t m, int nparts, int part, int64_t* row0, int64_t* rows);
+
+/* moa_plan — the static chooser (no device work; reads cached device props).
+ * device < 0 means the current device. */
+int moa_plan(int64_t m, int64_t n, int64_t p, int dtype, int device, moa_plan_t* out);
+
+/* moa_select_block_paper — the paper's own block arithmetic: the
+ * largest power-of-two side b with three b x b blocks (A, B, C) of
+ * elem_bytes each fitting l1_budget_bytes. 32 KiB, 8 -> 32; 128 KiB, 8 -> 64.
+ * Errors: MOA_ERR_INVALID_SHAPE if even b = 1 does not fit. */
+int moa_select_block_paper(int64_t l1_budget_bytes, int elem_bytes, int64_t* b);
+
+/* Communicator (library-owned; the 128-byte unique id is shipped by the caller,
+ * e.g. over torch.distributed). `device` is the CUDA device the rank uses. */
+int moa_comm_get_unique_id(unsigned char id[128]);
+int moa_comm_init(int nranks, int rank, const unsigned char id[128], int device, moa_comm_t* comm);
+int moa_comm_destroy(moa_comm_t comm);
+
+const char* moa_status_string(int status);
+const char* moa_last_error(void);
+int moa_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOA_H */

@@ -1,0 +1,288 @@
+"""B200-native MoA Operational-Normal-Form GEMM (arXiv 2306.11148) — Python binding.
+
+A thin ctypes layer over ``libmoa.so`` (C ABI in ``include/moa.h``). It only
+marshals arguments: every step of the GEMM runs in the library's sm_100a
+kernels. There is no CPU or PyTorch fallback — if the shared library is
+missing or fails to load, importing this package raises.
+
+PyTorch is used only for device memory, streams and process groups.
+
+    import paper_2306_11148_b200 as moa
+    C = moa.gemm(A, B)                      # C := A • B   (Eq. 3)
+    off, cnt = moa.psi([1], [2, 2])         # ψ: contiguous slice of rav ξ
+    r0, rows = moa.lift_rows(m, G, g)       # dimension lifting of the i axis
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+__all__ = [
+    "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
+    "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
+]
+
+F64, F32, F32_3XTF32 = 0, 1, 2
+KERNEL_NAMES = {0: "none", 1: "zero_fill", 2: "dgemm_tma", 3: "dgemm_generic", 4: "sgemm_ffma", 5: "sgemm_3xtf32"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libmoa.so")
+
+if not os.path.exists(lib_path):
+    raise ImportError(
+        f"{lib_path} not found: build it with `python tools/build.py moa` (or __graft_entry__.build()). "
+        "There is deliberately no fallback implementation.")
+_lib = ctypes.CDLL(lib_path)
+
+_i64, _i32, _vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+
+
+class _PlanT(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("bm", ctypes.c_int32), ("bn", ctypes.c_int32), ("bk", ctypes.c_int32),
+                ("stages", ctypes.c_int32), ("threads", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
+                ("grid", ctypes.c_int32), ("tiles_m", ctypes.c_int64), ("tiles_n", ctypes.c_int64),
+                ("tiles", ctypes.c_int64), ("raster_group", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("sms", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+def _sig(name, argtypes, restype=ctypes.c_int):
+    fn = getattr(_lib, name)
+    fn.argtypes = argtypes
+    fn.restype = restype
+    return fn
+
+
+_moa_gemm = _sig("moa_gemm", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
+_moa_gemm_with_plan = _sig("moa_gemm_with_plan", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, ctypes.POINTER(_PlanT), _vp])
+_moa_gemm_host = _sig("moa_gemm_host", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp])
+_moa_gemm_lifted = _sig("moa_gemm_lifted", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
+_moa_psi = _sig("moa_psi", [_i32, ctypes.POINTER(_i64), _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                            ctypes.POINTER(_i64)])
+_moa_lift_rows = _sig("moa_lift_rows", [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)])
+_moa_plan = _sig("moa_plan", [_i64, _i64, _i64, _i32, _i32, ctypes.POINTER(_PlanT)])
+_moa_select_block_paper = _sig("moa_select_block_paper", [_i64, _i32, ctypes.POINTER(_i64)])
+_moa_comm_get_unique_id = _sig("moa_comm_get_unique_id", [ctypes.c_char_p])
+_moa_comm_init = _sig("moa_comm_init", [_i32, _i32, ctypes.c_char_p, _i32, ctypes.POINTER(_vp)])
+_moa_comm_destroy = _sig("moa_comm_destroy", [_vp])
+_moa_status_string = _sig("moa_status_string", [_i32], ctypes.c_char_p)
+_moa_last_error = _sig("moa_last_error", [], ctypes.c_char_p)
+_moa_abi_version = _sig("moa_abi_version", [])
+
+
+class MoAError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        name = _moa_status_string(status).decode()
+        detail = (_moa_last_error() or b"").decode()
+        super().__init__(f"{where}: {name} ({detail})")
+        self.name = name
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise MoAError(rc, where)
+
+
+def abi_version() -> int:
+    return int(_moa_abi_version())
+
+
+# ----------------------------------------------------------------- helpers ---
+
+def psi(idx: Sequence[int], shape: Sequence[int]) -> tuple[int, int]:
+    """ψ(idx, ξ) on a row-major ξ of shape ``shape`` -> (offset, count) of rav ξ (moa.h)."""
+    r, q = len(shape), len(idx)
+    sh = (_i64 * max(r, 1))(*shape)
+    ix = (_i64 * max(q, 1))(*idx)
+    off, cnt = _i64(), _i64()
+    _check(_moa_psi(r, sh, q, ix, ctypes.byref(off), ctypes.byref(cnt)), "moa_psi")
+    return off.value, cnt.value
+
+
+def lift_rows(m: int, nparts: int, part: int) -> tuple[int, int]:
+    """Row lifting: (row0, rows) owned by ``part`` of ``nparts``."""
+    r0, r = _i64(), _i64()
+    _check(_moa_lift_rows(m, nparts, part, ctypes.byref(r0), ctypes.byref(r)), "moa_lift_rows")
+    return r0.value, r.value
+
+
+def select_block_paper(l1_budget_bytes: int, elem_bytes: int) -> int:
+    b = _i64()
+    _check(_moa_select_block_paper(l1_budget_bytes, elem_bytes, ctypes.byref(b)), "moa_select_block_paper")
+    return b.value
+
+
+@dataclass
+class Plan:
+    kernel: str
+    bm: int
+    bn: int
+    bk: int
+    stages: int
+    threads: int
+    ctas_per_sm: int
+    grid: int
+    tiles_m: int
+    tiles_n: int
+    tiles: int
+    raster_group: int
+    smem_bytes: int
+    sms: int
+
+    @classmethod
+    def _from(cls, p: _PlanT) -> "Plan":
+        return cls(KERNEL_NAMES.get(p.kernel, str(p.kernel)), p.bm, p.bn, p.bk, p.stages, p.threads, p.ctas_per_sm,
+                   p.grid, p.tiles_m, p.tiles_n, p.tiles, p.raster_group, p.smem_bytes, p.sms)
+
+    def _to(self) -> _PlanT:
+        inv = {v: k for k, v in KERNEL_NAMES.items()}
+        return _PlanT(inv[self.kernel], self.bm, self.bn, self.bk, self.stages, self.threads, self.ctas_per_sm,
+                      self.grid, self.tiles_m, self.tiles_n, self.tiles, self.raster_group, self.smem_bytes,
+                      self.sms, 0)
+
+
+def plan(m: int, n: int, p: int, dtype: int = F64, device: int = -1) -> Plan:
+    """The static block plan the library will use for an aligned (m, n, p) call."""
+    out = _PlanT()
+    _check(_moa_plan(m, n, p, dtype, device, ctypes.byref(out)), "moa_plan")
+    return Plan._from(out)
+
+
+# ------------------------------------------------------------------- gemm ---
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype} (float64 or float32)")
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _mat_check(A, B, out):
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0]:
+        raise ValueError(f"shape mismatch: rho A={tuple(A.shape)}, rho B={tuple(B.shape)} (Eq. 1, P:59-64)")
+    for name, t in (("A", A), ("B", B), ("out", out)):
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"{name} must be row-major contiguous (P:77-82)")
+        if t is not None and not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+    if A.dtype != B.dtype:
+        raise TypeError("A and B must share a dtype")
+
+
+def gemm(A, B, out=None, *, precision: Optional[str] = None, stream=None):
+    """C := A • B on the GPU (ONF, row-major contiguous). ``precision='3xtf32'`` selects
+    the TF32 tensor-core variant for float32 operands. Asynchronous on ``stream``."""
+    torch = _torch()
+    _mat_check(A, B, out)
+    m, n = A.shape
+    p = B.shape[1]
+    if out is None:
+        out = torch.empty((m, p), dtype=A.dtype, device=A.device)
+    elif tuple(out.shape) != (m, p) or out.dtype != A.dtype:
+        raise ValueError("out must be an m x p tensor of A's dtype")
+    code = _dtype_code(A)
+    if precision == "3xtf32":
+        if code != F32:
+            raise TypeError("3xtf32 needs float32 operands")
+        code = F32_3XTF32
+    _check(_moa_gemm(m, n, p, A.data_ptr() or None, B.data_ptr() or None, out.data_ptr() or None, code,
+                     _stream_ptr(stream)), "moa_gemm")
+    return out
+
+
+def gemm_with_plan(A, B, out, plan_: Plan, *, precision: Optional[str] = None, stream=None):
+    _mat_check(A, B, out)
+    m, n = A.shape
+    p = B.shape[1]
+    code = _dtype_code(A)
+    if precision == "3xtf32":
+        code = F32_3XTF32
+    pt = plan_._to()
+    _check(_moa_gemm_with_plan(m, n, p, A.data_ptr() or None, B.data_ptr() or None, out.data_ptr() or None, code,
+                               ctypes.byref(pt), _stream_ptr(stream)), "moa_gemm_with_plan")
+    return out
+
+
+def gemm_host(A_host, B_host, C_host, A_dev, B_dev, C_dev, *, precision: Optional[str] = None, stream=None):
+    """End-to-end C-ABI call on host buffers (pinned torch CPU tensors): H2D, GEMM, D2H, sync."""
+    m, n = A_host.shape
+    p = B_host.shape[1]
+    code = _dtype_code(A_host)
+    if precision == "3xtf32":
+        code = F32_3XTF32
+    for t in (A_host, B_host, C_host, A_dev, B_dev, C_dev):
+        if not t.is_contiguous():
+            raise ValueError("all buffers must be contiguous")
+    _check(_moa_gemm_host(m, n, p, A_host.data_ptr() or None, B_host.data_ptr() or None, C_host.data_ptr() or None,
+                          A_dev.data_ptr() or None, B_dev.data_ptr() or None, C_dev.data_ptr() or None, code,
+                          _stream_ptr(stream)), "moa_gemm_host")
+    return C_host
+
+
+# ------------------------------------------------------------ multi-GPU ----
+
+class Comm:
+    """Library-owned NCCL communicator; the 128-byte id travels over torch.distributed."""
+
+    def __init__(self, group=None, device: Optional[int] = None):
+        torch = _torch()
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else device
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(_moa_comm_get_unique_id(uid), "moa_comm_get_unique_id")
+        obj = [bytes(uid.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+        h = _vp()
+        _check(_moa_comm_init(self.world, self.rank, uid, self.device, ctypes.byref(h)), "moa_comm_init")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            _check(_moa_comm_destroy(self._h), "moa_comm_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precision: Optional[str] = None,
+                stream=None):
+    """Row-lifted C := A • B across the communicator (collective; see moa.h)."""
+    n = B.shape[0]
+    p = B.shape[1]
+    code = _dtype_code(B)
+    if precision == "3xtf32":
+        code = F32_3XTF32
+    for name, t in (("A_local", A_local), ("B", B), ("C_local", C_local), ("C_full", C_full)):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    _check(_moa_gemm_lifted(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None, C_local.data_ptr() or None,
+                            None if C_full is None else (C_full.data_ptr() or None), code, _stream_ptr(stream),
+                            comm.handle), "moa_gemm_lifted")
+    return C_local

@@ -1,0 +1,496 @@
+// moa_dgemm.cu — fp64 MoA-ONF GEMM kernels for sm_100a.
+//
+//   C[(i*p)+j] := sum_k A[(i*n)+k] * B[(k*p)+j]      (Eq. 3)
+//
+// K1 k_dgemm_tma   : persistent, warp-specialised. One producer warp streams the
+//                    operands with TMA (cp.async.bulk.tensor, 128B swizzle) into
+//                    an S-stage shared-memory ring guarded by mbarriers; 2..8
+//                    consumer warps run DMMA.8x8x4 (mma.sync m8n8k4 f64) on
+//                    register accumulators.
+// K2 k_dgemm_generic: same arithmetic, plain predicated loads (odd n or p,
+//                    pointers not 16-byte aligned — shapes TMA cannot describe).
+//
+// MoA mapping:
+//  * Dimension lifting: i -> (tile row tm, warp row wm, atom a, lane
+//    row); j -> (tile col tn, warp col wn, box bx, atom half h, lane col); the
+//    sigma loop is split into 16-wide k-slabs ("the sigma loop is broken up
+//    creating the block") whose partial sums stay in registers.
+//  * Contiguous access: A is staged as BM rows x 16 k of row-major
+//    segments (one 128 B run per row), B as 16 k-rows x 16 j boxes — rows of B,
+//    never columns (Fig. 1: scalar A[i,k] times row k of B). No
+//    transposed copy of anything exists.
+//  * Summation order: for every C element, k = 0,1,...,n-1 strictly ascending
+//    through k-slabs (ascending), DMMA k-steps (ascending) and the DMMA's
+//    internal chain (measured on B200: DMMA.8x8x4 == fma chain k0..k3,
+//    profiles/r01_fp64_probe.jsonl). Hence the result equals Fig. 3 ip.c with
+//    its update fused (reading R3) bit for bit, and it depends only on n — any
+//    row block computed alone equals the same rows of the full product.
+//  * Bank conflicts: the DMMA fragment rows/columns are permuted (rho, pi below)
+//    so that every ld.shared of a 128B-swizzled tile is conflict-free.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "moa_internal.h"
+
+namespace moa {
+namespace {
+
+// ------------------------------- PTX helpers --------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// Shared-memory fragment loads through plain C++ pointers into the __shared__
+// window: the compiler emits LDS.64 / LDS.128, may schedule them freely, and
+// still orders them after the mbarrier waits (which clobber "memory").
+__device__ __forceinline__ double lds64(const uint8_t* s, uint32_t off) {
+  return *reinterpret_cast<const double*>(s + off);
+}
+__device__ __forceinline__ double2 lds128(const uint8_t* s, uint32_t off) {
+  return *reinterpret_cast<const double2*>(s + off);
+}
+// D = A(8x4) * B(4x8) + C, fp64 tensor core. Lane l: a = A[l>>2][l&3],
+// b = B[l&3][l>>2], c/d = row l>>2, cols 2(l&3), 2(l&3)+1.
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Grouped rasterisation of output tiles (L2 reuse of A row-panels / B col-panels).
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n, int group, int64_t& tm,
+                                            int64_t& tn) {
+  const int64_t per_group = (int64_t)group * tiles_n;
+  const int64_t g = t / per_group;
+  const int64_t first = g * group;
+  const int64_t rem = tiles_m - first;
+  const int64_t gm = rem < group ? rem : group;
+  const int64_t r = t - g * per_group;
+  tm = first + r % gm;
+  tn = r / gm;
+}
+
+// ------------------------- shared-memory tile layout -------------------------
+// A stage: BM rows x 16 doubles (128 B per row), TMA SWIZZLE_128B: the 16-byte
+//   chunk c of row r lives at chunk c ^ (r & 7).
+// B stage: BN/16 boxes, each 16 k-rows x 16 doubles (2 KiB), same swizzle by k.
+constexpr int kBK = 16;
+constexpr int kRowBytes = kBK * 8;       // 128
+constexpr int kBoxBytes = 16 * kRowBytes;  // 2048
+
+// Per-lane fragment offsets (bytes), computed once.
+//  rho(g) = ((g&3)<<1)|(g>>2): MMA row g -> physical row inside the 8-row atom.
+//  pi(q)  = (q>>1)|((q&1)<<2): MMA col q -> physical 2-double pair inside a box;
+//           the "even" atom takes the pair's first double, the "odd" atom the second.
+struct FragOffsets {
+  uint32_t a[4];  // per k-step s (4 per k-slab)
+  uint32_t b[2];  // per (s & 1); add s*512 for the k-row base
+  int rr;         // rho(lane>>2)
+  int t;          // lane & 3
+};
+__device__ __forceinline__ FragOffsets make_offsets(int lane) {
+  FragOffsets f;
+  const int g = lane >> 2, t = lane & 3;
+  const int rr = ((g & 3) << 1) | (g >> 2);
+  const int piq = (g >> 1) | ((g & 1) << 2);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) f.a[s] = rr * kRowBytes + ((((2 * s) + (t >> 1)) ^ rr) << 4) + ((t & 1) << 3);
+#pragma unroll
+  for (int s = 0; s < 2; ++s) f.b[s] = t * kRowBytes + ((piq ^ (4 * s + t)) << 4);
+  f.rr = rr;
+  f.t = t;
+  return f;
+}
+
+template <int NBOX>
+struct Acc {
+  double v[4][NBOX][2][2];  // [A atom][box][even/odd atom][C pair]
+};
+
+template <int NBOX>
+__device__ __forceinline__ void acc_zero(Acc<NBOX>& c) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) c.v[a][b][h][0] = c.v[a][b][h][1] = 0.0;
+}
+
+// One 16-wide k-slab: 4 k-steps (ascending) x (4 x 2*NBOX) DMMA atoms.
+// a_base: this warp's 32 rows of the A stage; b_base: its first B box.
+template <int NBOX>
+__device__ __forceinline__ void mma_slab(Acc<NBOX>& c, const uint8_t* a_base, const uint8_t* b_base,
+                                         const FragOffsets& f) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    double af[4];
+    double2 bf[NBOX];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) af[a] = lds64(a_base, a * 8 * kRowBytes + f.a[s]);
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b) bf[b] = lds128(b_base, b * kBoxBytes + s * 4 * kRowBytes + f.b[s & 1]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b) {
+        dmma(c.v[a][b][0], af[a], bf[b].x);
+        dmma(c.v[a][b][1], af[a], bf[b].y);
+      }
+  }
+}
+
+// Write the warp's 32 x (16*NBOX) block of C. Lane holds, for atom a and box b,
+// row rho(g) and columns {2t, 2t+1} (pair 0) and {2t+8, 2t+9} (pair 1).
+template <int NBOX, bool kVec>
+__device__ __forceinline__ void store_acc(const Acc<NBOX>& c, double* __restrict__ C, int64_t m, int64_t p,
+                                          int64_t row0, int64_t col0, const FragOffsets& f) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t r = row0 + a * 8 + f.rr;
+    if (r >= m) continue;
+    double* crow = C + r * p;
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t col = col0 + b * 16 + 2 * f.t + 8 * q;
+        const double lo = c.v[a][b][0][q], hi = c.v[a][b][1][q];
+        if (kVec) {
+          if (col < p) *reinterpret_cast<double2*>(crow + col) = make_double2(lo, hi);
+        } else {
+          if (col < p) crow[col] = lo;
+          if (col + 1 < p) crow[col + 1] = hi;
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------- K1: TMA + WS --------------------------------
+// Register file is split per SM sub-partition (warp w -> SMSP w % 4, 16384
+// registers each). With 8 consumer warps a lone producer warp would put 3 warps
+// on one SMSP and cap every thread at 168 registers (the 64 fp64 accumulators
+// alone need 128), so the producer becomes a full warpgroup that gives its
+// registers to the consumers with setmaxnreg: per SMSP 1 x 40 + 2 x 232 regs.
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+struct K1Traits {
+  static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
+  static constexpr int kProducerWarps = kConsumerWarps >= 8 ? 4 : 1;
+  static constexpr bool kSetMaxNReg = kProducerWarps == 4;
+  static constexpr int kProducerRegs = 40;
+  static constexpr int kConsumerRegs = 232;
+  static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
+  static_assert(!kSetMaxNReg || (kProducerRegs + 2 * kConsumerRegs) * 32 <= 16384, "per-SMSP register budget");
+  static constexpr int kNBox = BN / WARPS_N / 16;
+  static constexpr int kABytes = BM * kRowBytes;
+  static constexpr int kBBytes = BN * kRowBytes;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8;
+  static_assert(BM == 32 * WARPS_M, "warp tile is 32 rows");
+  static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
+};
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
+__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
+    k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n,
+                int group) {
+  using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
+  const uint8_t* sptr = smem_raw + (sbase - raw);
+  const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
+  const uint32_t empty0 = full0 + STAGES * 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles = tiles_m * tiles_n;
+  const int ktiles = (int)((n + kBK - 1) / kBK);
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp >= Tr::kConsumerWarps) {
+    // ----------------------------- producer ---------------------------------
+    if constexpr (Tr::kSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Tr::kProducerRegs));
+    if (warp == Tr::kConsumerWarps && lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t tm, tn;
+        tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+        const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_arrive_expect_tx(fb, Tr::kStageBytes);
+          const uint32_t sa = sbase + stage * Tr::kStageBytes;
+          tma_load_2d(sa, &tmA, fb, kt * kBK, row0);
+#pragma unroll
+          for (int b = 0; b < BN / 16; ++b) tma_load_2d(sa + Tr::kABytes + b * kBoxBytes, &tmB, fb, col0 + 16 * b, kt * kBK);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------- consumers ---------------------------------
+  if constexpr (Tr::kSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Tr::kConsumerRegs));
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const FragOffsets f = make_offsets(lane);
+  Acc<Tr::kNBox> acc;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int64_t tm, tn;
+    tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+    acc_zero(acc);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      mbar_wait(full0 + 8 * stage, phase);
+      const uint8_t* sa = sptr + stage * Tr::kStageBytes;
+      mma_slab(acc, sa + wm * 32 * kRowBytes, sa + Tr::kABytes + wn * Tr::kNBox * kBoxBytes, f);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    store_acc<Tr::kNBox, true>(acc, C, m, p, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
+  }
+}
+
+// ------------------------------ K2: generic ----------------------------------
+template <int BM, int BN, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
+    k_dgemm_generic(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int64_t m,
+                    int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n, int group) {
+  constexpr int kNBox = BN / WARPS_N / 16;
+  constexpr int kThreads = WARPS_M * WARPS_N * 32;
+  __shared__ __align__(1024) uint8_t sm[(BM + BN) * kRowBytes];
+  const uint8_t* sa = sm;
+  const uint8_t* sb = sm + BM * kRowBytes;
+  double* sA = reinterpret_cast<double*>(sm);
+  double* sB = reinterpret_cast<double*>(sm + BM * kRowBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const FragOffsets f = make_offsets(lane);
+  const int64_t tiles = tiles_m * tiles_n;
+  Acc<kNBox> acc;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    int64_t tm, tn;
+    tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+    const int64_t row0 = tm * BM, col0 = tn * BN;
+    acc_zero(acc);
+    for (int64_t k0 = 0; k0 < n; k0 += kBK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < BM * kBK; e += kThreads) {  // A: row r, k
+        const int r = e / kBK, k = e % kBK;
+        const int64_t gi = row0 + r, gk = k0 + k;
+        const double v = (gi < m && gk < n) ? A[gi * n + gk] : 0.0;
+        sA[(r * kRowBytes + (((k >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3)) / 8] = v;
+      }
+      for (int e = threadIdx.x; e < kBK * BN; e += kThreads) {  // B: k-row, col
+        const int k = e / BN, c = e % BN;
+        const int64_t gk = k0 + k, gj = col0 + c;
+        const double v = (gk < n && gj < p) ? B[gk * p + gj] : 0.0;
+        const int box = c >> 4, cc = c & 15;
+        sB[(box * kBoxBytes + k * kRowBytes + (((cc >> 1) ^ (k & 7)) << 4) + ((cc & 1) << 3)) / 8] = v;
+      }
+      __syncthreads();
+      mma_slab(acc, sa + wm * 32 * kRowBytes, sb + wn * kNBox * kBoxBytes, f);
+    }
+    store_acc<kNBox, false>(acc, C, m, p, row0 + wm * 32, col0 + wn * kNBox * 16, f);
+  }
+}
+
+// ------------------------------ host helpers ---------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp64 row-major tensor map: dims {cols (inner), rows}, box {16, box_rows}, 128B swizzle.
+bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled entry point unavailable");
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+    set_error(buf);
+    return false;
+  }
+  return true;
+}
+
+template <int BM, int BN, int WM, int WN, int ST>
+int launch_k1(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A, const double* B, double* C,
+              cudaStream_t stream) {
+  using Tr = K1Traits<BM, BN, WM, WN, ST>;
+  CUtensorMap ta, tb;
+  if (!encode_2d_f64(&ta, A, m, n, BM) || !encode_2d_f64(&tb, B, n, p, 16)) return MOA_ERR_CUDA;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST>;
+  static std::once_flag once;  // per instantiation
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    return MOA_ERR_CUDA;
+  }
+  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n,
+                                                       plan.raster_group);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
+    return MOA_ERR_CUDA;
+  }
+  return MOA_OK;
+}
+
+// The chooser's candidate lifted blocks. ctas_per_sm is refined at first use
+// from the occupancy API (registers are what limit it; see K1Traits).
+TileConfig kK1Configs[] = {
+    // kernel, bm, bn, bk, stages, threads, ctas/SM, smem, eta
+    {MOA_KERNEL_DGEMM_TMA, 128, 128, 16, 6, K1Traits<128, 128, 4, 2, 6>::kThreads, 1, K1Traits<128, 128, 4, 2, 6>::kSmem, 1.00},
+    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 1, 4>::kThreads, 1, K1Traits<128, 64, 4, 1, 4>::kSmem, 0.97},
+    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 2, 4>::kThreads, 2, K1Traits<64, 64, 2, 2, 4>::kSmem, 0.93},
+};
+TileConfig kK2Configs[] = {
+    {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
+};
+
+template <int BM, int BN, int WM, int WN, int ST>
+int k1_occupancy() {
+  using Tr = K1Traits<BM, BN, WM, WN, ST>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Tr::kThreads, Tr::kSmem) != cudaSuccess) return 0;
+  return n;
+}
+
+void refine_occupancy() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int o[3] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 1, 4>(), k1_occupancy<64, 64, 2, 2, 4>()};
+    for (int i = 0; i < 3; ++i)
+      if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
+      kK2Configs[0].ctas_per_sm = n;
+    cudaGetLastError();
+  });
+}
+
+}  // namespace
+
+int dgemm_tile_configs(int kernel, const TileConfig** out) {
+  refine_occupancy();
+  if (kernel == MOA_KERNEL_DGEMM_TMA) {
+    *out = kK1Configs;
+    return (int)(sizeof(kK1Configs) / sizeof(kK1Configs[0]));
+  }
+  if (kernel == MOA_KERNEL_DGEMM_GENERIC) {
+    *out = kK2Configs;
+    return 1;
+  }
+  *out = nullptr;
+  return 0;
+}
+
+int launch_dgemm_tma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A, const double* B,
+                     double* C, cudaStream_t stream) {
+  if (plan.bm == 128 && plan.bn == 128 && plan.stages == 6) return launch_k1<128, 128, 4, 2, 6>(plan, m, n, p, A, B, C, stream);
+  if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 1, 4>(plan, m, n, p, A, B, C, stream);
+  if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 2, 4>(plan, m, n, p, A, B, C, stream);
+  set_error("no compiled K1 instance for this plan");
+  return MOA_ERR_INVALID_SHAPE;
+}
+
+int launch_dgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A,
+                         const double* B, double* C, cudaStream_t stream) {
+  k_dgemm_generic<64, 64, 2, 2><<<plan.grid, 128, 0, stream>>>(A, B, C, m, n, p, plan.tiles_m, plan.tiles_n,
+                                                             plan.raster_group);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_dgemm_generic launch: ") + cudaGetErrorString(e));
+    return MOA_ERR_CUDA;
+  }
+  return MOA_OK;
+}
+
+}  // namespace moa

@@ -1,0 +1,542 @@
+// moa_host.cpp — the C-ABI host layer of libmoa.so (declared in include/moa.h):
+// argument validation, the static block plan, psi / row-lifting helpers,
+// kernel dispatch, the NCCL-backed row-lifted path and error reporting.
+//
+// Paper references: PAPER.md lines P:n (see include/moa.h for the per-entry
+// citations). Readings R1..R16: DESIGN.md §Readings.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "moa.h"
+#include "moa_internal.h"
+
+struct moa_comm_s {
+  ncclComm_t nccl = nullptr;
+  int nranks = 0;
+  int rank = 0;
+  int device = 0;
+};
+
+namespace moa {
+
+namespace {
+thread_local std::string g_last_error;
+
+std::mutex g_dev_mu;
+std::map<int, DeviceShape> g_devs;
+
+int elem_size(int dtype) {
+  switch (dtype) {
+    case MOA_F64: return 8;
+    case MOA_F32: return 4;
+    case MOA_F32_3XTF32: return 4;
+    default: return 0;
+  }
+}
+
+bool mul_ok(int64_t a, int64_t b, int64_t* out) {
+  return !__builtin_mul_overflow(a, b, out);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return MOA_ERR_CUDA;
+}
+
+int get_device_shape(int device, DeviceShape* out) {
+  if (device < 0) {
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_devs.find(device);
+    if (it != g_devs.end()) {
+      *out = it->second;
+      return MOA_OK;
+    }
+  }
+  DeviceShape d;
+  d.device = device;
+  cudaError_t e;
+  int v = 0;
+  if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
+    return cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+  cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+  cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  cudaDeviceGetAttribute(&d.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&d.regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device);
+  d.l2_bytes = v;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  g_devs[device] = d;
+  *out = d;
+  return MOA_OK;
+}
+
+// Validation shared by moa_gemm / moa_gemm_lifted / moa_gemm_host (before any CUDA call).
+int validate(int64_t m, int64_t n, int64_t p, const void* A, const void* B, const void* C, int dtype) {
+  if (m < 0 || n < 0 || p < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  const int es = elem_size(dtype);
+  if (es == 0) {
+    set_error("unknown dtype");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  int64_t mn, np_, mp, t;
+  if (!mul_ok(m, n, &mn) || !mul_ok(n, p, &np_) || !mul_ok(m, p, &mp) || !mul_ok(mn, es, &t) ||
+      !mul_ok(np_, es, &t) || !mul_ok(mp, es, &t)) {
+    set_error("extent product overflows int64");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if ((mn > 0 && !A) || (np_ > 0 && !B) || (mp > 0 && !C)) {
+    set_error("NULL pointer for a non-empty operand");
+    return MOA_ERR_NULL_POINTER;
+  }
+  auto mis = [es](const void* q) { return q && (reinterpret_cast<uintptr_t>(q) % (uintptr_t)es) != 0; };
+  if (mis(A) || mis(B) || mis(C)) {
+    set_error("pointer not aligned to the element size");
+    return MOA_ERR_MISALIGNED;
+  }
+  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
+    if (xb <= 0 || yb <= 0) return false;
+    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
+    return a0 < b1 && b0 < a1;
+  };
+  if (overlap(C, mp * es, A, mn * es) || overlap(C, mp * es, B, np_ * es)) {
+    set_error("C overlaps A or B (':=' needs a distinct output)");
+    return MOA_ERR_ALIASING;
+  }
+  return MOA_OK;
+}
+
+// Is this call describable by the TMA kernels? (strides multiple of 16 B, bases
+// 16-B aligned, coordinates fit the tensor map's int32.)
+bool tma_eligible(int64_t m, int64_t n, int64_t p, const void* A, const void* B, const void* C, int es) {
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  const int per16 = 16 / es;
+  return (n % per16 == 0) && (p % per16 == 0) && al16(A) && al16(B) && al16(C) && m < INT32_MAX && n < INT32_MAX &&
+         p < INT32_MAX;
+}
+
+// The static chooser: among the compiled tile configs of
+// `kernel`, pick the one with the best predicted SM-level efficiency
+//   eff = (m*p) / (waves * sms * bm*bn) * eta,   waves = ceil(tiles / sms),
+// i.e. the lifted block (bm x bn) "as close as possible" to filling every SM's
+// fp64 pipe for a whole number of waves. No measurement, no autotuning.
+int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* out) {
+  const TileConfig* cfgs = nullptr;
+  int nc = 0;
+  if (kernel == MOA_KERNEL_DGEMM_TMA || kernel == MOA_KERNEL_DGEMM_GENERIC)
+    nc = dgemm_tile_configs(kernel, &cfgs);
+  else
+    nc = sgemm_tile_configs(kernel, &cfgs);
+  if (nc <= 0) {
+    set_error("no tile configuration compiled for this kernel");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  double best = -1.0;
+  int bi = 0;
+  for (int i = 0; i < nc; ++i) {
+    const TileConfig& c = cfgs[i];
+    if (c.smem_bytes > ds.smem_optin) continue;
+    const int64_t tm = (m + c.bm - 1) / c.bm, tn = (p + c.bn - 1) / c.bn, tiles = tm * tn;
+    const int64_t waves = (tiles + ds.sms - 1) / ds.sms;
+    const double eff = (double)m * (double)p / ((double)waves * ds.sms * (double)c.bm * c.bn) * c.eta;
+    if (eff > best + 1e-12) {
+      best = eff;
+      bi = i;
+    }
+  }
+  const TileConfig& c = cfgs[bi];
+  memset(out, 0, sizeof(*out));
+  out->kernel = c.kernel;
+  out->bm = c.bm;
+  out->bn = c.bn;
+  out->bk = c.bk;
+  out->stages = c.stages;
+  out->threads = c.threads;
+  out->ctas_per_sm = c.ctas_per_sm;
+  out->tiles_m = (m + c.bm - 1) / c.bm;
+  out->tiles_n = (p + c.bn - 1) / c.bn;
+  out->tiles = out->tiles_m * out->tiles_n;
+  const int64_t slots = (int64_t)ds.sms * c.ctas_per_sm;
+  out->grid = (int32_t)(out->tiles < slots ? out->tiles : slots);
+  out->raster_group = (int32_t)(out->tiles_m < 8 ? out->tiles_m : 8);
+  if (out->raster_group < 1) out->raster_group = 1;
+  out->smem_bytes = c.smem_bytes;
+  out->sms = ds.sms;
+  return MOA_OK;
+}
+
+int plan_impl(int64_t m, int64_t n, int64_t p, int dtype, const DeviceShape& ds, bool tma_ok, moa_plan_t* out) {
+  memset(out, 0, sizeof(*out));
+  out->sms = ds.sms;
+  if (m == 0 || p == 0) {
+    out->kernel = MOA_KERNEL_NONE;
+    return MOA_OK;
+  }
+  if (n == 0) {
+    out->kernel = MOA_KERNEL_ZERO_FILL;
+    return MOA_OK;
+  }
+  int kernel;
+  if (dtype == MOA_F64)
+    kernel = tma_ok ? MOA_KERNEL_DGEMM_TMA : MOA_KERNEL_DGEMM_GENERIC;
+  else if (dtype == MOA_F32)
+    kernel = MOA_KERNEL_SGEMM_FFMA;
+  else if (dtype == MOA_F32_3XTF32)
+    kernel = MOA_KERNEL_SGEMM_3XTF32;
+  else {
+    set_error("unknown dtype");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  return choose(kernel, m, p, ds, out);
+}
+
+int check_device(const DeviceShape& ds) {
+  if (ds.cc_major != 10 || ds.cc_minor != 0) {
+    set_error("libmoa.so is compiled for sm_100a only (B200); device is sm_" + std::to_string(ds.cc_major) +
+              std::to_string(ds.cc_minor));
+    return MOA_ERR_UNSUPPORTED_DEVICE;
+  }
+  return MOA_OK;
+}
+
+int run_plan(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C,
+             int dtype, cudaStream_t s) {
+  switch (plan.kernel) {
+    case MOA_KERNEL_NONE: return MOA_OK;
+    case MOA_KERNEL_ZERO_FILL: {
+      cudaError_t e = cudaMemsetAsync(C, 0, (size_t)(m * p * elem_size(dtype)), s);
+      return e == cudaSuccess ? MOA_OK : cuda_fail(e, "cudaMemsetAsync");
+    }
+    case MOA_KERNEL_DGEMM_TMA:
+      return launch_dgemm_tma(plan, m, n, p, (const double*)A, (const double*)B, (double*)C, s);
+    case MOA_KERNEL_DGEMM_GENERIC:
+      return launch_dgemm_generic(plan, m, n, p, (const double*)A, (const double*)B, (double*)C, s);
+    case MOA_KERNEL_SGEMM_FFMA:
+      return launch_sgemm_ffma(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
+    case MOA_KERNEL_SGEMM_3XTF32:
+      return launch_sgemm_3xtf32(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
+    default: set_error("bad plan kernel id"); return MOA_ERR_INVALID_SHAPE;
+  }
+}
+
+ncclDataType_t nccl_type(int dtype) { return dtype == MOA_F64 ? ncclFloat64 : ncclFloat32; }
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  set_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return MOA_ERR_NCCL;
+}
+
+}  // namespace
+
+void set_error(const std::string& s) { g_last_error = s; }
+
+}  // namespace moa
+
+using namespace moa;
+
+extern "C" {
+
+int moa_abi_version(void) { return MOA_ABI_VERSION; }
+
+const char* moa_last_error(void) { return g_last_error.c_str(); }
+
+const char* moa_status_string(int status) {
+  switch (status) {
+    case MOA_OK: return "MOA_OK";
+    case MOA_ERR_INVALID_SHAPE: return "MOA_ERR_INVALID_SHAPE";
+    case MOA_ERR_INVALID_DTYPE: return "MOA_ERR_INVALID_DTYPE";
+    case MOA_ERR_NULL_POINTER: return "MOA_ERR_NULL_POINTER";
+    case MOA_ERR_ALIASING: return "MOA_ERR_ALIASING";
+    case MOA_ERR_MISALIGNED: return "MOA_ERR_MISALIGNED";
+    case MOA_ERR_INVALID_INDEX: return "MOA_ERR_INVALID_INDEX";
+    case MOA_ERR_CUDA: return "MOA_ERR_CUDA";
+    case MOA_ERR_NCCL: return "MOA_ERR_NCCL";
+    case MOA_ERR_UNSUPPORTED_DEVICE: return "MOA_ERR_UNSUPPORTED_DEVICE";
+    default: return "MOA_ERR_UNKNOWN";
+  }
+}
+
+int moa_psi(int rank, const int64_t* shape, int q, const int64_t* idx, int64_t* offset, int64_t* count) {
+  if (!offset || !count || (rank > 0 && !shape) || (q > 0 && !idx)) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (rank < 0 || q < 0 || q > rank) {
+    set_error("index longer than the shape");
+    return MOA_ERR_INVALID_INDEX;
+  }
+  for (int d = 0; d < rank; ++d)
+    if (shape[d] < 0) {
+      set_error("negative extent");
+      return MOA_ERR_INVALID_SHAPE;
+    }
+  for (int d = 0; d < q; ++d)
+    if (idx[d] < 0 || idx[d] >= shape[d]) {
+      set_error("index out of bounds (0 <=* i <* rho xi)");
+      return MOA_ERR_INVALID_INDEX;
+    }
+  // count = pi(shape[q..rank)); offset = gamma_row(idx ++ zeros) by Horner.
+  int64_t cnt = 1;
+  for (int d = q; d < rank; ++d)
+    if (!mul_ok(cnt, shape[d], &cnt)) {
+      set_error("shape product overflows int64");
+      return MOA_ERR_INVALID_SHAPE;
+    }
+  int64_t off = 0;
+  for (int d = 0; d < rank; ++d) {
+    const int64_t i = d < q ? idx[d] : 0;
+    if (!mul_ok(off, shape[d], &off) || __builtin_add_overflow(off, i, &off)) {
+      set_error("offset overflows int64");
+      return MOA_ERR_INVALID_SHAPE;
+    }
+  }
+  if (cnt == 0) off = 0;
+  *offset = off;
+  *count = cnt;
+  return MOA_OK;
+}
+
+int moa_lift_rows(int64_t m, int nparts, int part, int64_t* row0, int64_t* rows) {
+  if (!row0 || !rows) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (m < 0 || nparts <= 0 || part < 0 || part >= nparts) {
+    set_error("bad row-lifting arguments");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  const int64_t q = m / nparts, r = m % nparts;
+  *rows = q + (part < r ? 1 : 0);
+  *row0 = (int64_t)part * q + (part < r ? part : r);
+  return MOA_OK;
+}
+
+int moa_select_block_paper(int64_t l1_budget_bytes, int elem_bytes, int64_t* b) {
+  if (!b) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (elem_bytes <= 0 || l1_budget_bytes < 3LL * elem_bytes) {
+    set_error("budget too small for three 1x1 blocks");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t s = 1;
+  while (s < (1LL << 30) && 3 * (2 * s) * (2 * s) * (int64_t)elem_bytes <= l1_budget_bytes) s *= 2;
+  *b = s;
+  return MOA_OK;
+}
+
+int moa_plan(int64_t m, int64_t n, int64_t p, int dtype, int device, moa_plan_t* out) {
+  if (!out) {
+    set_error("NULL plan");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (m < 0 || n < 0 || p < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if (elem_size(dtype) == 0) {
+    set_error("unknown dtype");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  DeviceShape ds;
+  int rc = get_device_shape(device, &ds);
+  if (rc) return rc;
+  const int per16 = 16 / elem_size(dtype);
+  const bool tma_ok = n % per16 == 0 && p % per16 == 0 && m < INT32_MAX && n < INT32_MAX && p < INT32_MAX;
+  return plan_impl(m, n, p, dtype, ds, tma_ok, out);
+}
+
+int moa_gemm_with_plan(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype,
+                       const moa_plan_t* plan, void* stream) {
+  int rc = validate(m, n, p, A, B, C, dtype);
+  if (rc) return rc;
+  DeviceShape ds;
+  if ((rc = get_device_shape(-1, &ds))) return rc;
+  if ((rc = check_device(ds))) return rc;
+  const bool tma_ok = tma_eligible(m, n, p, A, B, C, elem_size(dtype));
+  moa_plan_t pl;
+  if ((rc = plan_impl(m, n, p, dtype, ds, tma_ok, &pl))) return rc;
+  if (plan && pl.kernel == plan->kernel) {
+    // honour an explicit tile choice (the block-size experiment) if it is a compiled config
+    const TileConfig* cfgs = nullptr;
+    int nc = (pl.kernel == MOA_KERNEL_DGEMM_TMA || pl.kernel == MOA_KERNEL_DGEMM_GENERIC)
+                 ? dgemm_tile_configs(pl.kernel, &cfgs)
+                 : sgemm_tile_configs(pl.kernel, &cfgs);
+    bool found = false;
+    for (int i = 0; i < nc; ++i)
+      if (cfgs[i].bm == plan->bm && cfgs[i].bn == plan->bn && cfgs[i].stages == plan->stages) {
+        pl.bm = cfgs[i].bm;
+        pl.bn = cfgs[i].bn;
+        pl.stages = cfgs[i].stages;
+        pl.threads = cfgs[i].threads;
+        pl.ctas_per_sm = cfgs[i].ctas_per_sm;
+        pl.smem_bytes = cfgs[i].smem_bytes;
+        pl.tiles_m = (m + pl.bm - 1) / pl.bm;
+        pl.tiles_n = (p + pl.bn - 1) / pl.bn;
+        pl.tiles = pl.tiles_m * pl.tiles_n;
+        const int64_t slots = (int64_t)ds.sms * pl.ctas_per_sm;
+        pl.grid = (int32_t)(pl.tiles < slots ? pl.tiles : slots);
+        if (plan->grid > 0 && plan->grid < pl.grid) pl.grid = plan->grid;
+        if (plan->raster_group > 0) pl.raster_group = plan->raster_group;
+        found = true;
+      }
+    if (!found) {
+      set_error("requested tile configuration is not compiled");
+      return MOA_ERR_INVALID_SHAPE;
+    }
+  } else if (plan) {
+    set_error("plan kernel does not match the kernel this call requires");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  return run_plan(pl, m, n, p, A, B, C, dtype, (cudaStream_t)stream);
+}
+
+int moa_gemm(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype, void* stream) {
+  return moa_gemm_with_plan(m, n, p, A, B, C, dtype, nullptr, stream);
+}
+
+int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
+                  void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream) {
+  int rc = validate(m, n, p, A_dev, B_dev, C_dev, dtype);
+  if (rc) return rc;
+  const int64_t es = elem_size(dtype);
+  if ((m * n > 0 && !A_host) || (n * p > 0 && !B_host) || (m * p > 0 && !C_host)) {
+    set_error("NULL host pointer for a non-empty operand");
+    return MOA_ERR_NULL_POINTER;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (m * n > 0 && (e = cudaMemcpyAsync(A_dev, A_host, (size_t)(m * n * es), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "H2D A");
+  if (n * p > 0 && (e = cudaMemcpyAsync(B_dev, B_host, (size_t)(n * p * es), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "H2D B");
+  if ((rc = moa_gemm(m, n, p, A_dev, B_dev, C_dev, dtype, stream))) return rc;
+  if (m * p > 0 && (e = cudaMemcpyAsync(C_host, C_dev, (size_t)(m * p * es), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "D2H C");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return MOA_OK;
+}
+
+int moa_comm_get_unique_id(unsigned char id[128]) {
+  if (!id) {
+    set_error("NULL id");
+    return MOA_ERR_NULL_POINTER;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(id, &u, 128);
+  return MOA_OK;
+}
+
+int moa_comm_init(int nranks, int rank, const unsigned char id[128], int device, moa_comm_t* comm) {
+  if (!id || !comm) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (nranks <= 0 || rank < 0 || rank >= nranks) {
+    set_error("bad rank/nranks");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  auto* c = new moa_comm_s;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  *comm = c;
+  return MOA_OK;
+}
+
+int moa_comm_destroy(moa_comm_t comm) {
+  if (!comm) return MOA_OK;
+  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  delete comm;
+  return r == ncclSuccess ? MOA_OK : nccl_fail(r, "ncclCommDestroy");
+}
+
+int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
+                    int dtype, void* stream, moa_comm_t comm) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  int64_t row0 = 0, rows = 0;
+  int rc = moa_lift_rows(m < 0 ? 0 : m, comm->nranks, comm->rank, &row0, &rows);
+  if (m < 0) rc = MOA_ERR_INVALID_SHAPE;
+  if (rc) return rc;
+  if ((rc = validate(rows, n, p, A_local, B, C_local, dtype))) return rc;
+  const int64_t es = elem_size(dtype);
+  if (C_full && (reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
+    set_error("C_full not aligned to the element size");
+    return MOA_ERR_MISALIGNED;
+  }
+  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
+    if (!x || !y || xb <= 0 || yb <= 0) return false;
+    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
+    return a0 < b1 && b0 < a1;
+  };
+  if (C_full && (overlap(C_full, m * p * es, B, n * p * es) || overlap(C_full, m * p * es, A_local, rows * n * es) ||
+                 overlap(C_full, m * p * es, C_local, rows * p * es))) {
+    set_error("C_full overlaps another operand");
+    return MOA_ERR_ALIASING;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const ncclDataType_t ty = nccl_type(dtype);
+  // (1) every processor needs all of B (ip_rows.c reads B[(sigma*sizer)+j] with no
+  //     processor index): in-place broadcast from rank 0 over NVLink.
+  if (n * p > 0 && comm->nranks > 1) {
+    ncclResult_t r = ncclBroadcast(B, B, (size_t)(n * p), ty, 0, comm->nccl, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B)");
+  }
+  // (2) the lifted compute: this rank's rows of C (Fig. 4, k = rank).
+  if ((rc = moa_gemm(rows, n, p, A_local, B, C_local, dtype, stream))) return rc;
+  // (3) optional gather of C (reading R14).
+  if (C_full && m * p > 0) {
+    if (comm->nranks == 1) {
+      cudaError_t e = cudaMemcpyAsync(C_full, C_local, (size_t)(m * p * es), cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(C_full)");
+    } else if (m % comm->nranks == 0) {
+      ncclResult_t r = ncclAllGather(C_local, C_full, (size_t)(rows * p), ty, comm->nccl, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(C)");
+    } else {
+      ncclResult_t r = ncclGroupStart();
+      for (int g = 0; g < comm->nranks && r == ncclSuccess; ++g) {
+        int64_t r0, rg;
+        moa_lift_rows(m, comm->nranks, g, &r0, &rg);
+        if (rg == 0) continue;
+        r = ncclBroadcast(g == comm->rank ? C_local : nullptr, (char*)C_full + r0 * p * es, (size_t)(rg * p), ty, g,
+                          comm->nccl, s);
+      }
+      ncclResult_t r2 = ncclGroupEnd();
+      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(C block)");
+      if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+    }
+  }
+  return MOA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// moa_internal.h — product-internal interface between the C-ABI host layer
+// (moa_host.cpp) and the kernel translation units. Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "moa.h"
+
+namespace moa {
+
+// Per-device properties the static plan reads (cached, mutex-guarded).
+struct DeviceShape {
+  int device = -1;
+  int sms = 0;
+  int cc_major = 0, cc_minor = 0;
+  int smem_optin = 0;          // sharedMemPerBlockOptin
+  int smem_per_sm = 0;         // sharedMemPerMultiprocessor
+  int regs_per_sm = 0;
+  int64_t l2_bytes = 0;
+};
+
+// Thread-local error detail for moa_last_error().
+void set_error(const std::string& s);
+
+// Kernel launchers (moa_dgemm.cu / moa_sgemm.cu). Arguments are validated by the
+// host layer; the plan is a valid output of plan_*(). Return a moa_status.
+int launch_dgemm_tma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A, const double* B,
+                     double* C, cudaStream_t stream);
+int launch_dgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A,
+                         const double* B, double* C, cudaStream_t stream);
+int launch_sgemm_ffma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
+                      float* C, cudaStream_t stream);
+int launch_sgemm_3xtf32(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A,
+                        const float* B, float* C, cudaStream_t stream);
+
+// Static tile configurations compiled into the library (the chooser's candidates).
+struct TileConfig {
+  int kernel;
+  int bm, bn, bk, stages, threads, ctas_per_sm, smem_bytes;
+  double eta;  // per-tile efficiency prior (smaller tiles: more smem/L2 traffic per flop)
+};
+// Return the number of configs for a kernel id and fill *out (static storage).
+int dgemm_tile_configs(int kernel, const TileConfig** out);  // moa_dgemm.cu
+int sgemm_tile_configs(int kernel, const TileConfig** out);  // moa_sgemm.cu
+
+}  // namespace moa

@@ -1,0 +1,245 @@
+"""GPU parity of the fp64 MoA-ONF GEMM (C ABI via the binding) against the CPU oracle.
+
+Bars (north_star + DESIGN.md §Parity):
+  * bitwise vs oracle ``ip(fused=True)`` (Fig. 3 ip.c with the update fused,
+    reading R3) on ANY finite input — the kernels keep k strictly ascending and
+    DMMA.8x8x4 is an fma chain (profiles/r01_fp64_probe.jsonl);
+  * bitwise vs the unfused literal ip.c on integer-valued inputs;
+  * relative Frobenius error vs the unfused literal ip.c <= 1e-12 * sqrt(n).
+Large shapes (the bench configs) are checked on sampled rows (rows of C are
+independent, Fig. 1 / P:99) plus a Freivalds product check.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from inputs import inputs as I
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257]
+
+
+def _moa():
+    import paper_2306_11148_b200 as moa
+    return moa
+
+
+def _host(m, n, p, seed, kind=I.UNIFORM, dtype=np.float64):
+    A = I.host_matrix(m, n, seed, I.ID_A, kind, dtype)
+    B = I.host_matrix(n, p, seed, I.ID_B, kind, dtype)
+    return A, B
+
+
+def _gpu_gemm(A, B, dev, precision=None):
+    import torch
+    tA = torch.from_numpy(A).to(dev)
+    tB = torch.from_numpy(B).to(dev)
+    C = _moa().gemm(tA, tB, precision=precision)
+    torch.cuda.synchronize()
+    return C.cpu().numpy()
+
+
+def _bits_equal(x, y):
+    # == semantics (±0 equal), and no NaNs expected
+    return x.shape == y.shape and bool(np.all(x == y))
+
+
+def _relfro(x, ref):
+    d = np.linalg.norm((x - ref).ravel())
+    r = np.linalg.norm(ref.ravel())
+    return d / r if r > 0 else d
+
+
+def test_config0_square_256_vs_oracle(cuda_device):
+    """BASELINE configs[0]: m=n=p=256 fp64 against the full oracle, seeds 1-3."""
+    for seed in (1, 2, 3):
+        A, B = _host(256, 256, 256, seed)
+        C = _gpu_gemm(A, B, cuda_device)
+        assert _bits_equal(C, O.ip(A, B, fused=True)), seed
+        assert _relfro(C, O.ip(A, B, fused=False)) <= 1e-12 * np.sqrt(256)
+        Ai, Bi = _host(256, 256, 256, seed, kind=I.INT)
+        assert _bits_equal(_gpu_gemm(Ai, Bi, cuda_device), O.ip(Ai, Bi, fused=False))
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_tile_edge_shapes(cuda_device, seed):
+    """Shapes straddling every tile/box/atom edge, even (TMA kernel) and odd (generic kernel)."""
+    rng = np.random.default_rng(100 + seed)
+    shapes = {(m, n, p) for m in (1, 129, 257) for n in (1, 17, 64) for p in (2, 130, 256)}
+    shapes |= {tuple(int(x) for x in rng.choice(EDGE, size=3)) for _ in range(30)}
+    for (m, n, p) in sorted(shapes):
+        A, B = _host(m, n, p, seed)
+        C = _gpu_gemm(A, B, cuda_device)
+        assert _bits_equal(C, O.ip(A, B, fused=True)), (m, n, p)
+        assert _relfro(C, O.ip(A, B, fused=False)) <= 1e-12 * np.sqrt(n), (m, n, p)
+
+
+def test_generic_kernel_on_misaligned_pointers(cuda_device):
+    """Element-aligned but not 16-byte aligned operands route to the generic kernel:
+    same bits."""
+    import torch
+    moa = _moa()
+    m, n, p = 70, 46, 38
+    A, B = _host(m, n, p, 4)
+    bufA = torch.empty(m * n + 1, dtype=torch.float64, device=cuda_device)
+    bufB = torch.empty(n * p + 1, dtype=torch.float64, device=cuda_device)
+    bufC = torch.empty(m * p + 1, dtype=torch.float64, device=cuda_device)
+    tA = bufA[1:].view(m, n)
+    tB = bufB[1:].view(n, p)
+    tC = bufC[1:].view(m, p)
+    tA.copy_(torch.from_numpy(A))
+    tB.copy_(torch.from_numpy(B))
+    moa.gemm(tA, tB, out=tC)
+    torch.cuda.synchronize()
+    assert _bits_equal(tC.cpu().numpy(), O.ip(A, B, fused=True))
+
+
+def test_identities_bitwise(cuda_device):
+    m, n, p = 200, 96, 130
+    A, B = _host(m, n, p, 5)
+    assert _bits_equal(_gpu_gemm(A, np.eye(n), cuda_device), A)
+    assert _bits_equal(_gpu_gemm(np.eye(m), A, cuda_device), A)
+    assert _bits_equal(_gpu_gemm(A, np.zeros((n, p)), cuda_device), np.zeros((m, p)))
+    C = _gpu_gemm(A, B, cuda_device)
+    Ct = _gpu_gemm(np.ascontiguousarray(B.T), np.ascontiguousarray(A.T), cuda_device)
+    assert _bits_equal(C.T, Ct)  # products commute exactly, same k order
+
+
+def test_rank1_closed_form(cuda_device):
+    rng = np.random.default_rng(6)
+    m, n, p = 300, 250, 170
+    u, z = rng.integers(-2, 3, size=m), rng.integers(-2, 3, size=p)
+    v, w = rng.integers(-1, 2, size=n), rng.integers(-1, 2, size=n)
+    A, B = np.outer(u, v).astype(np.float64), np.outer(w, z).astype(np.float64)
+    C = _gpu_gemm(A, B, cuda_device)
+    assert _bits_equal(C, np.outer(u, z).astype(np.float64) * float(v @ w))
+
+
+def test_zero_extents(cuda_device):
+    import torch
+    moa = _moa()
+    A = torch.empty((5, 0), dtype=torch.float64, device=cuda_device)
+    B = torch.empty((0, 7), dtype=torch.float64, device=cuda_device)
+    C = torch.full((5, 7), 3.0, dtype=torch.float64, device=cuda_device)
+    moa.gemm(A, B, out=C)
+    torch.cuda.synchronize()
+    assert torch.all(C == 0)
+    A0 = torch.empty((0, 4), dtype=torch.float64, device=cuda_device)
+    B0 = torch.ones((4, 3), dtype=torch.float64, device=cuda_device)
+    assert moa.gemm(A0, B0).shape == (0, 3)
+
+
+def test_aliasing_rejected(cuda_device):
+    import torch
+    moa = _moa()
+    A = torch.ones((64, 64), dtype=torch.float64, device=cuda_device)
+    B = torch.ones((64, 64), dtype=torch.float64, device=cuda_device)
+    with pytest.raises(moa.MoAError) as e:
+        moa.gemm(A, B, out=A)
+    assert e.value.name == "MOA_ERR_ALIASING"
+
+
+def test_row_block_invariance_and_determinism(cuda_device):
+    """F8: any row block computed alone is bitwise the same rows of the full product,
+    and two runs are bitwise equal (no atomics, k order fixed by n alone)."""
+    import torch
+    moa = _moa()
+    m, n, p = 1000, 520, 384
+    A, B = _host(m, n, p, 7)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    full = moa.gemm(tA, tB)
+    again = moa.gemm(tA, tB)
+    torch.cuda.synchronize()
+    assert torch.equal(full, again)
+    for (r0, r1) in [(0, 1), (0, 500), (333, 1000), (999, 1000), (128, 256), (7, 700)]:
+        part = moa.gemm(tA[r0:r1].contiguous(), tB)
+        torch.cuda.synchronize()
+        assert torch.equal(part, full[r0:r1]), (r0, r1)
+
+
+def test_each_compiled_tile_config_bitwise(cuda_device):
+    """The block-size sweep configs (the paper's block-size experiment) all compute the
+    same bits — the plan changes only the lifting, never the k order."""
+    import torch
+    moa = _moa()
+    m, n, p = 300, 200, 260
+    A, B = _host(m, n, p, 8)
+    ref = O.ip(A, B, fused=True)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    base = moa.plan(m, n, p)
+    assert base.kernel == "dgemm_tma"
+    for (bm, bn, st) in [(128, 128, 6), (128, 64, 4), (64, 64, 4)]:
+        pl = moa.Plan(**{**base.__dict__, "bm": bm, "bn": bn, "stages": st})
+        out = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+        moa.gemm_with_plan(tA, tB, out, pl)
+        torch.cuda.synchronize()
+        assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
+
+
+def test_plan_is_static_and_sane(cuda_device):
+    moa = _moa()
+    for (m, n, p) in [(256, 256, 256), (1024, 1024, 1024), (8192, 8192, 8192), (16384, 16384, 16384),
+                      (65536, 512, 512)]:
+        pl = moa.plan(m, n, p)
+        assert pl.kernel == "dgemm_tma" and pl.bk == 16
+        assert pl.tiles == -(-m // pl.bm) * -(-p // pl.bn)
+        assert 1 <= pl.grid <= pl.sms * pl.ctas_per_sm and pl.ctas_per_sm >= 1
+        assert moa.plan(m, n, p) == pl
+    assert moa.plan(16384, 16384, 16384).bm == 128
+    assert moa.plan(5, 7, 9).kernel == "dgemm_generic"  # odd n / p: not describable by TMA
+
+
+def _freivalds(Ct, tA, tB, trials=2):
+    """y = C x vs z = A (B x) on the GPU in fp64 with x in {+-1}^p: O(N^2) check of every element."""
+    import torch
+    worst = 0.0
+    for t in range(trials):
+        g = torch.Generator(device="cpu").manual_seed(1234 + t)
+        x = (torch.randint(0, 2, (Ct.shape[1], 1), generator=g) * 2 - 1).to(Ct)
+        y = Ct @ x
+        z = tA @ (tB @ x)
+        worst = max(worst, float(torch.linalg.norm(y - z) / torch.linalg.norm(z)))
+    return worst
+
+
+@pytest.mark.parametrize("cfg", ["square8192", "skinny65536x512"])
+def test_bench_configs_sampled_rows(cuda_device, cfg):
+    """At the full BASELINE sizes in the launch configuration bench.py times: sampled rows
+    bitwise vs the oracle (tile-boundary rows included) + Freivalds on the whole of C."""
+    import torch
+    moa = _moa()
+    m, n, p = (8192, 8192, 8192) if cfg == "square8192" else (65536, 512, 512)
+    seed = 1
+    tA = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+    tB = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+    I.device_fill(tA, seed, I.ID_A)
+    I.device_fill(tB, seed, I.ID_B)
+    C = moa.gemm(tA, tB)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    rows = sorted({0, m - 1, 127, 128, 129, m // 2, m // 2 + 1, *rng.integers(0, m, size=9).tolist()})
+    B = I.host_matrix(n, p, seed, I.ID_B)
+    Arows = I.host_rows(rows, n, seed, I.ID_A)
+    ref = O.ip_rowblock(Arows, B, fused=True)
+    got = C[torch.tensor(rows, device=cuda_device)].cpu().numpy()
+    assert _bits_equal(got, ref)
+    assert _freivalds(C, tA, tB) <= 1e-12 * np.sqrt(n)
+
+
+def test_gemm_host_e2e(cuda_device):
+    """moa_gemm_host: host buffers in, host result out, same bits."""
+    import torch
+    moa = _moa()
+    m, n, p = 333, 128, 210
+    A, B = _host(m, n, p, 9)
+    hA = torch.from_numpy(A).pin_memory()
+    hB = torch.from_numpy(B).pin_memory()
+    hC = torch.empty((m, p), dtype=torch.float64).pin_memory()
+    dA = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+    dB = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+    dC = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+    moa.gemm_host(hA, hB, hC, dA, dB, dC)
+    assert _bits_equal(hC.numpy(), O.ip(A, B, fused=True))
