@@ -21,6 +21,7 @@ host's cores on a bounded row sample), energy (NVML joules per GEMM), an N sweep
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
 import statistics
@@ -82,10 +83,9 @@ class ClockSampler:
         import torch
         nv = self.nv
         try:  # map CUDA device -> NVML by PCI bus id (CUDA_VISIBLE_DEVICES order != NVML order)
-            bus = torch.cuda.get_device_properties(device_index).pci_bus_id if hasattr(
-                torch.cuda.get_device_properties(device_index), "pci_bus_id") else None
-            if bus:
-                return nv.nvmlDeviceGetHandleByPciBusId(bus.encode() if isinstance(bus, str) else bus)
+            pr = torch.cuda.get_device_properties(device_index)
+            bus = "%08X:%02X:%02X.0" % (int(pr.pci_domain_id), int(pr.pci_bus_id), int(pr.pci_device_id))
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
         except Exception:
             pass
         return nv.nvmlDeviceGetHandleByIndex(device_index)
@@ -212,6 +212,7 @@ def run_reference(args):
 # ----------------------------------------------------------------- GPU arm --
 
 def main():
+    faulthandler.enable()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
