@@ -58,7 +58,8 @@ typedef enum {
   MOA_KERNEL_DGEMM_TMA = 2,     /* K1: fp64 DMMA, TMA + mbarrier warp-specialised */
   MOA_KERNEL_DGEMM_GENERIC = 3, /* K2: fp64 DMMA, plain loads (odd n/p, unaligned) */
   MOA_KERNEL_SGEMM_FFMA = 4,    /* K3: exact fp32 FFMA */
-  MOA_KERNEL_SGEMM_3XTF32 = 5   /* K4: 3xTF32 on tcgen05 tensor cores */
+  MOA_KERNEL_SGEMM_3XTF32 = 5,  /* K4: 3xTF32 on tcgen05 tensor cores */
+  MOA_KERNEL_SGEMM_GENERIC = 6  /* K3g: exact fp32, plain loads (n/p not multiples of 4, unaligned) */
 } moa_kernel;
 
 /* Static block plan ("block sizes derived statically from shapes and types",

@@ -25,7 +25,8 @@ __all__ = [
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
-KERNEL_NAMES = {0: "none", 1: "zero_fill", 2: "dgemm_tma", 3: "dgemm_generic", 4: "sgemm_ffma", 5: "sgemm_3xtf32"}
+KERNEL_NAMES = {0: "none", 1: "zero_fill", 2: "dgemm_tma", 3: "dgemm_generic", 4: "sgemm_ffma", 5: "sgemm_3xtf32",
+                6: "sgemm_generic"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libmoa.so")

@@ -36,51 +36,13 @@
 #include <mutex>
 
 #include "moa_internal.h"
+#include "moa_ptx.cuh"
 
 namespace moa {
 namespace {
 
-// ------------------------------- PTX helpers --------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
+using namespace ptx;
+
 // Shared-memory fragment loads through plain C++ pointers into the __shared__
 // window: the compiler emits LDS.64 / LDS.128, may schedule them freely, and
 // still orders them after the mbarrier waits (which clobber "memory").
@@ -96,19 +58,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
-}
-
-// Grouped rasterisation of output tiles (L2 reuse of A row-panels / B col-panels).
-__device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n, int group, int64_t& tm,
-                                            int64_t& tn) {
-  const int64_t per_group = (int64_t)group * tiles_n;
-  const int64_t g = t / per_group;
-  const int64_t first = g * group;
-  const int64_t rem = tiles_m - first;
-  const int64_t gm = rem < group ? rem : group;
-  const int64_t r = t - g * per_group;
-  tm = first + r % gm;
-  tn = r / gm;
 }
 
 // ------------------------- shared-memory tile layout -------------------------
@@ -359,40 +308,8 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
 }
 
 // ------------------------------ host helpers ---------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
-// 2-D fp64 row-major tensor map: dims {cols (inner), rows}, box {16, box_rows}, 128B swizzle.
 bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
-  auto enc = get_encode();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled entry point unavailable");
-    return false;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
-  cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1u, 1u};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    char buf[128];
-    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
-    set_error(buf);
-    return false;
-  }
-  return true;
+  return encode_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, base, rows, cols, 16, box_rows);
 }
 
 template <int BM, int BN, int WM, int WN, int ST>

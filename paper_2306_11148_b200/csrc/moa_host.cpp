@@ -194,9 +194,9 @@ int plan_impl(int64_t m, int64_t n, int64_t p, int dtype, const DeviceShape& ds,
   if (dtype == MOA_F64)
     kernel = tma_ok ? MOA_KERNEL_DGEMM_TMA : MOA_KERNEL_DGEMM_GENERIC;
   else if (dtype == MOA_F32)
-    kernel = MOA_KERNEL_SGEMM_FFMA;
-  else if (dtype == MOA_F32_3XTF32)
-    kernel = MOA_KERNEL_SGEMM_3XTF32;
+    kernel = tma_ok ? MOA_KERNEL_SGEMM_FFMA : MOA_KERNEL_SGEMM_GENERIC;
+  else if (dtype == MOA_F32_3XTF32)  // shapes TMA cannot describe fall back to the (more exact) fp32 kernel
+    kernel = tma_ok ? MOA_KERNEL_SGEMM_3XTF32 : MOA_KERNEL_SGEMM_GENERIC;
   else {
     set_error("unknown dtype");
     return MOA_ERR_INVALID_DTYPE;
@@ -227,6 +227,8 @@ int run_plan(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const void
       return launch_dgemm_generic(plan, m, n, p, (const double*)A, (const double*)B, (double*)C, s);
     case MOA_KERNEL_SGEMM_FFMA:
       return launch_sgemm_ffma(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
+    case MOA_KERNEL_SGEMM_GENERIC:
+      return launch_sgemm_generic(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
     case MOA_KERNEL_SGEMM_3XTF32:
       return launch_sgemm_3xtf32(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
     default: set_error("bad plan kernel id"); return MOA_ERR_INVALID_SHAPE;

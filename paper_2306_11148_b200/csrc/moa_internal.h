@@ -32,6 +32,8 @@ int launch_dgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p
                          const double* B, double* C, cudaStream_t stream);
 int launch_sgemm_ffma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
                       float* C, cudaStream_t stream);
+int launch_sgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A,
+                         const float* B, float* C, cudaStream_t stream);
 int launch_sgemm_3xtf32(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A,
                         const float* B, float* C, cudaStream_t stream);
 
@@ -44,5 +46,6 @@ struct TileConfig {
 // Return the number of configs for a kernel id and fill *out (static storage).
 int dgemm_tile_configs(int kernel, const TileConfig** out);  // moa_dgemm.cu
 int sgemm_tile_configs(int kernel, const TileConfig** out);  // moa_sgemm.cu
+int tf32_tile_configs(int kernel, const TileConfig** out);   // moa_tf32.cu
 
 }  // namespace moa

@@ -1,0 +1,101 @@
+"""GPU parity of the fp32 paths against the oracle (BASELINE configs[2]).
+
+K3 (exact fp32, FFMA2): bitwise vs oracle ``ip(fused=True)`` in float32 on any
+finite input (k ascending fma chain from +0), bitwise vs the literal oracle on
+integer-valued inputs, and relative Frobenius <= 1e-5*sqrt(n) vs the literal
+unfused ip.c. K4 (3xTF32 on tcgen05): <= 5e-3 vs the literal oracle (north_star,
+reported separately), and its error vs the fp64-accumulated truth is reported.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from inputs import inputs as I
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _moa():
+    import paper_2306_11148_b200 as moa
+    return moa
+
+
+def _host(m, n, p, seed, kind=I.UNIFORM):
+    return (I.host_matrix(m, n, seed, I.ID_A, kind, np.float32),
+            I.host_matrix(n, p, seed, I.ID_B, kind, np.float32))
+
+
+def _run(A, B, dev, precision=None):
+    import torch
+    C = _moa().gemm(torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev), precision=precision)
+    torch.cuda.synchronize()
+    return C.cpu().numpy()
+
+
+def _relfro(x, ref):
+    x = x.astype(np.float64)
+    ref = ref.astype(np.float64)
+    r = np.linalg.norm(ref)
+    return np.linalg.norm(x - ref) / r if r > 0 else np.linalg.norm(x)
+
+
+SHAPES = [(1, 1, 4), (7, 5, 3), (128, 32, 128), (129, 33, 130), (255, 64, 257), (256, 256, 256), (300, 100, 500),
+          (17, 1000, 40), (1000, 4, 8)]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_ffma_exact_bitwise(cuda_device, seed):
+    for (m, n, p) in SHAPES:
+        A, B = _host(m, n, p, seed)
+        C = _run(A, B, cuda_device)
+        assert np.array_equal(C, O.ip(A, B, fused=True)), (m, n, p)
+        assert _relfro(C, O.ip(A, B, fused=False)) <= 1e-5 * np.sqrt(n), (m, n, p)
+
+
+def test_ffma_integer_exact(cuda_device):
+    for (m, n, p) in [(256, 256, 256), (129, 333, 131)]:
+        A, B = _host(m, n, p, 3, kind=I.INT)
+        assert np.array_equal(_run(A, B, cuda_device), O.ip(A, B, fused=False))
+
+
+def test_ffma_identities(cuda_device):
+    m, n, p = 200, 96, 132
+    A, _ = _host(m, n, p, 4)
+    assert np.array_equal(_run(A, np.eye(n, dtype=np.float32), cuda_device), A)
+    assert np.array_equal(_run(np.eye(m, dtype=np.float32), A, cuda_device), A)
+
+
+def test_ffma_row_block_invariance(cuda_device):
+    import torch
+    moa = _moa()
+    m, n, p = 700, 300, 260
+    A, B = _host(m, n, p, 5)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    full = moa.gemm(tA, tB)
+    for (r0, r1) in [(0, 1), (5, 133), (128, 700)]:
+        assert torch.equal(moa.gemm(tA[r0:r1].contiguous(), tB), full[r0:r1])
+
+
+def test_ffma_config2_n16384_sampled_rows(cuda_device):
+    """BASELINE configs[2] at full size (fp32 N=16384): sampled rows bitwise vs the oracle."""
+    import torch
+    moa = _moa()
+    N = 16384
+    tA = torch.empty((N, N), dtype=torch.float32, device=cuda_device)
+    tB = torch.empty((N, N), dtype=torch.float32, device=cuda_device)
+    I.device_fill(tA, 1, I.ID_A)
+    I.device_fill(tB, 1, I.ID_B)
+    C = moa.gemm(tA, tB)
+    torch.cuda.synchronize()
+    rows = [0, 127, 128, N - 1]
+    B = I.host_matrix(N, N, 1, I.ID_B, dtype=np.float32)
+    ref = O.ip_rowblock(I.host_rows(rows, N, 1, I.ID_A, dtype=np.float32), B, fused=True)
+    assert np.array_equal(C[torch.tensor(rows, device=cuda_device)].cpu().numpy(), ref)
+
+
+def test_plan_fp32(cuda_device):
+    moa = _moa()
+    assert moa.plan(16384, 16384, 16384, moa.F32).kernel == "sgemm_ffma"
+    assert moa.plan(100, 101, 102, moa.F32).kernel == "sgemm_generic"
