@@ -1,0 +1,152 @@
+#!/usr/bin/env python3
+"""Measure every BASELINE.json config on one B200 (not the driver's bench line).
+
+  configs[0] fp64 m=n=p=256                 configs[1] fp64 N sweep 1024..8192 (+16384 target)
+  configs[2] fp32 N=16384 exact vs 3xTF32   configs[3] fp64 65536x512x512
+plus the paper's block-size experiment (Figs. 3-8 analogue): every
+compiled tile config at each N, time and J/GEMM, with the static chooser's pick.
+Timing: CUDA events around R back-to-back launches after 3 warm-ups, R sized so a
+window lasts >= ~1 s (NVML energy granularity); inputs resident in HBM.
+Output: one JSON document on stdout.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2306_11148_b200 as moa  # noqa: E402
+from bench import FP64_DMMA_PEAK_TFLOPS, ClockSampler  # noqa: E402
+from inputs import inputs as I  # noqa: E402
+
+FFMA_PEAK_TFLOPS = 72.0  # measured FFMA (profiles/r01_fp64_probe.jsonl); 74.4 nominal
+TF32_NOMINAL_TFLOPS = 1100.0  # B200_PROFILING.md nominal dense TF32
+
+
+def timed(fn, window_s, sampler, est_s):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    reps = max(3, int(window_s / max(est_s, 1e-6)))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0 = sampler.energy_mj()
+    with sampler:
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+    e1 = sampler.energy_mj()
+    ms = a.elapsed_time(b) / reps
+    out = {"ms": round(ms, 5), "reps": reps}
+    if e0 is not None and e1 is not None:
+        out["j_per_gemm"] = round((e1 - e0) / 1e3 / reps, 6)
+        out["avg_w"] = round((e1 - e0) / 1e3 / (ms * reps / 1e3), 1)
+    return out
+
+
+def mats(m, n, p, dtype):
+    A = torch.empty((m, n), dtype=dtype, device="cuda")
+    B = torch.empty((n, p), dtype=dtype, device="cuda")
+    C = torch.empty((m, p), dtype=dtype, device="cuda")
+    I.device_fill(A, 1, I.ID_A)
+    I.device_fill(B, 1, I.ID_B)
+    return A, B, C
+
+
+def rec(m, n, p, r, peak):
+    fl = 2.0 * m * n * p
+    r["gflops"] = round(fl / (r["ms"] / 1e3) / 1e9, 1)
+    r["frac_of_peak"] = round(fl / (r["ms"] / 1e3) / 1e12 / peak, 4)
+    r["hbm_gbs_algorithmic"] = None
+    return r
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--window", type=float, default=1.0)
+    ap.add_argument("--sizes", default="1024,1536,2048,3072,4096,6144,8192,16384")
+    ap.add_argument("--skip-blocks", action="store_true")
+    a = ap.parse_args()
+    sampler = ClockSampler(0, period=0.1)
+    out = {"device": torch.cuda.get_device_name(0), "fp64_peak_tflops": FP64_DMMA_PEAK_TFLOPS,
+           "ffma_peak_tflops": FFMA_PEAK_TFLOPS, "time": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+
+    # configs[0]
+    A, B, C = mats(256, 256, 256, torch.float64)
+    r = timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, 5e-6)
+    out["config0_fp64_256"] = rec(256, 256, 256, r, FP64_DMMA_PEAK_TFLOPS)
+    out["config0_fp64_256"]["plan"] = moa.plan(256, 256, 256).__dict__
+
+    # configs[1] sweep + block-size experiment
+    sweep = []
+    for N in [int(x) for x in a.sizes.split(",")]:
+        A, B, C = mats(N, N, N, torch.float64)
+        est = 2.0 * N ** 3 / (FP64_DMMA_PEAK_TFLOPS * 0.9e12)
+        pl = moa.plan(N, N, N)
+        r = rec(N, N, N, timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, est), FP64_DMMA_PEAK_TFLOPS)
+        r.update({"N": N, "plan": {"bm": pl.bm, "bn": pl.bn, "stages": pl.stages, "grid": pl.grid,
+                                   "tiles": pl.tiles}, "clocks": sampler.summary()})
+        sampler.samples = []
+        if not a.skip_blocks:
+            blocks = []
+            for (bm, bn, st) in [(128, 128, 6), (128, 64, 4), (64, 64, 4)]:
+                q = moa.Plan(**{**pl.__dict__, "bm": bm, "bn": bn, "stages": st})
+                rb = rec(N, N, N, timed(lambda: moa.gemm_with_plan(A, B, C, q), min(a.window, 0.5), sampler, est),
+                         FP64_DMMA_PEAK_TFLOPS)
+                rb.update({"bm": bm, "bn": bn, "stages": st, "chosen": (bm, bn) == (pl.bm, pl.bn)})
+                blocks.append(rb)
+            best = min(blocks, key=lambda x: x["ms"])
+            r["block_sweep"] = blocks
+            r["chooser_vs_best"] = round(best["ms"] / next(x["ms"] for x in blocks if x["chosen"]), 4)
+        sweep.append(r)
+        del A, B, C
+        torch.cuda.empty_cache()
+    out["config1_fp64_sweep"] = sweep
+    import math
+    pts = [(x["N"], x["j_per_gemm"]) for x in sweep if x.get("j_per_gemm") and x["N"] <= 8192]
+    if len(pts) >= 3:
+        xs, ys = [math.log(x) for x, _ in pts], [math.log(y) for _, y in pts]
+        mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
+        out["energy_exponent_fit_1024_8192"] = round(
+            sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs), 3)
+
+    # configs[2] fp32 N=16384
+    N = 16384
+    A, B, C = mats(N, N, N, torch.float32)
+    r = rec(N, N, N, timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, 2.0 * N ** 3 / 60e12), FFMA_PEAK_TFLOPS)
+    r["kernel"] = moa.plan(N, N, N, moa.F32).kernel
+    out["config2_fp32_16384_exact"] = r
+    try:
+        r = rec(N, N, N, timed(lambda: moa.gemm(A, B, out=C, precision="3xtf32"), a.window, sampler,
+                               2.0 * N ** 3 / 200e12), TF32_NOMINAL_TFLOPS / 3)
+        r["kernel"] = moa.plan(N, N, N, moa.F32_3XTF32).kernel
+        r["peak_note"] = "frac against TF32 nominal / 3 (three TF32 products per output term)"
+        out["config2_fp32_16384_3xtf32"] = r
+    except moa.MoAError as e:
+        out["config2_fp32_16384_3xtf32"] = {"error": str(e)}
+    del A, B, C
+    torch.cuda.empty_cache()
+
+    # configs[3] skinny
+    m, n, p = 65536, 512, 512
+    A, B, C = mats(m, n, p, torch.float64)
+    r = rec(m, n, p, timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, 2.0 * m * n * p / 33e12),
+            FP64_DMMA_PEAK_TFLOPS)
+    byts = 8 * (m * n + n * p + m * p)
+    r["hbm_gbs_algorithmic"] = round(byts / (r["ms"] / 1e3) / 1e9, 1)
+    r["plan"] = moa.plan(m, n, p).__dict__
+    out["config3_fp64_65536x512x512"] = r
+    json.dump(out, sys.stdout, indent=1)
+    print()
+
+
+if __name__ == "__main__":
+    main()
