@@ -1,15 +1,330 @@
-// moa_tf32.cu — K4: fp32 GEMM as 3xTF32 on tcgen05 tensor cores (placeholder
-// until the kernel lands; the dtype reports MOA_ERR_INVALID_DTYPE meanwhile).
+// moa_tf32.cu — K4: fp32 MoA-ONF GEMM as 3xTF32 on the 5th-generation tensor
+// cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM).
+//
+//   C[(i*p)+j] := sum_k A[(i*n)+k] * B[(k*p)+j]      (Eq. 3)
+//   computed as  Ab*Bb + Ab*Bs + As*Bb,  x = xb + xs,  xb = x & 0xFFFFE000 (exact
+//   in TF32), xs = x - xb (exact in fp32)  — north_star's "documented TF32/3xTF32
+//   tensor-core variant"; NOT exact (tolerance 5e-3, reported separately).
+//
+// Structure (persistent, one CTA per SM, 128 x 128 output tiles, k-slabs of 32):
+//   warp 0      TMA producer: A row segments (128 rows x 32 floats, K-major) and
+//               B row segments (32 k-rows x 32-float boxes, MN-major — B is used
+//               exactly as stored, row-major, never transposed: Fig. 1) into
+//               a raw ring.
+//   warps 2..5  converters: raw slab -> (big, small) slabs, same swizzled layout
+//               (the split is elementwise, so no index math), then
+//               fence.proxy.async so the tensor core sees the generic writes.
+//   warp 1      TMEM allocator + MMA issuer (one thread): per k-step of 8,
+//               3 x tcgen05.mma (M=128, N=128, K=8) into a TMEM accumulator;
+//               tcgen05.commit frees the split slab / publishes the tile.
+//   warps 6..9  epilogue: tcgen05.ld 32x32b -> registers -> global (row-major C).
+// Accumulators are double-buffered in TMEM (2 x 128 columns) so the epilogue of
+// tile t overlaps the MMAs of tile t+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+
 #include "moa_internal.h"
+#include "moa_ptx.cuh"
 
 namespace moa {
-int tf32_tile_configs(int, const TileConfig** out) {
+namespace {
+using namespace ptx;
+
+constexpr int kBM = 128, kBN = 128, kBK = 32;  // floats
+constexpr int kRowBytes = kBK * 4;              // 128
+constexpr int kABytes = kBM * kRowBytes;        // 16 KiB
+constexpr int kBBox = 32 * kRowBytes;           // 32 k-rows x 32 floats = 4 KiB
+constexpr int kBBytes = (kBN / 32) * kBBox;     // 16 KiB
+constexpr int kRawBytes = kABytes + kBBytes;    // 32 KiB
+constexpr int kSplitBytes = 2 * kRawBytes;      // big A, big B, small A, small B
+constexpr int kRawStages = 2, kSplitStages = 2;
+constexpr int kAccCols = kBN;                   // fp32 accumulator columns per buffer
+constexpr int kTmemCols = 2 * kAccCols;         // double buffered
+constexpr int kThreads = 10 * 32;
+constexpr int kConvThreads = 128;
+// barriers: raw_full/raw_empty[2], split_full/split_empty[2], acc_full/acc_empty[2]
+constexpr int kSmem = 1024 + kRawStages * kRawBytes + kSplitStages * kSplitBytes + 12 * 8 + 16;
+
+// ---------------------------- tcgen05 helpers ----------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor: D fp32 (c_format=1 @4), A,B tf32 (=2 @7, @10), A K-major
+// (bit15=0), B MN-major (bit16=1), N>>3 @17, M>>4 @24.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                            ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sgemm_3xtf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n,
+                   int group) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw0 = smem_u32(smem_raw);
+  const uint32_t base = (raw0 + 1023u) & ~1023u;
+  uint8_t* sptr = smem_raw + (base - raw0);
+  const uint32_t raw_s = base;                                   // raw ring
+  const uint32_t split_s = base + kRawStages * kRawBytes;        // split ring
+  const uint32_t bars = split_s + kSplitStages * kSplitBytes;
+  const uint32_t raw_full = bars, raw_empty = bars + 16, split_full = bars + 32, split_empty = bars + 48;
+  const uint32_t acc_full = bars + 64, acc_empty = bars + 80;
+  const uint32_t tmem_slot = bars + 96;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles = tiles_m * tiles_n;
+  const int ktiles = (int)((n + kBK - 1) / kBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(raw_full + 8 * s, 1);
+      mbar_init(raw_empty + 8 * s, kConvThreads / 32);
+      mbar_init(split_full + 8 * s, kConvThreads / 32);
+      mbar_init(split_empty + 8 * s, 1);
+      mbar_init(acc_full + 8 * s, 1);
+      mbar_init(acc_empty + 8 * s, 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sptr + (tmem_slot - base));
+
+  if (warp == 0) {
+    // ------------------------------- TMA producer -------------------------------
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t tm, tn;
+        tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          mbar_wait(raw_empty + 8 * st, ph ^ 1u);
+          const uint32_t fb = raw_full + 8 * st;
+          mbar_arrive_expect_tx(fb, kRawBytes);
+          const uint32_t dst = raw_s + st * kRawBytes;
+          tma_load_2d(dst, &tmA, fb, kt * kBK, (int)(tm * kBM));
+#pragma unroll
+          for (int b = 0; b < kBN / 32; ++b)
+            tma_load_2d(dst + kABytes + b * kBBox, &tmB, fb, (int)(tn * kBN) + 32 * b, kt * kBK);
+          if (++st == kRawStages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------- MMA issuer --------------------------------
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(acc_empty + 8 * ab, aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(ab * kAccCols);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          mbar_wait(split_full + 8 * st, ph);
+          tc_fence_after();
+          const uint32_t s0 = split_s + st * kSplitBytes;
+          const uint32_t a_big = s0, b_big = s0 + kABytes, a_sml = s0 + kRawBytes, b_sml = s0 + kRawBytes + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            // A: K-major, k-step of 8 floats = 32 B inside the 128 B swizzle row; SBO = 8 rows.
+            const uint64_t dAb = smem_desc(a_big + kk * 32, 16, 1024);
+            const uint64_t dAs = smem_desc(a_sml + kk * 32, 16, 1024);
+            // B: MN-major, k-step of 8 rows = 1024 B; LBO = next 32-column box, SBO = 8 rows.
+            const uint64_t dBb = smem_desc(b_big + kk * 1024, kBBox, 1024);
+            const uint64_t dBs = smem_desc(b_sml + kk * 1024, kBBox, 1024);
+            const uint32_t acc0 = (kt > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(d, dAs, dBb, kIdesc, acc0);
+            mma_tf32(d, dAb, dBs, kIdesc, 1u);
+            mma_tf32(d, dAb, dBb, kIdesc, 1u);
+          }
+          tc_commit(split_empty + 8 * st);  // slab consumed once these MMAs complete
+          if (++st == kSplitStages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+        tc_commit(acc_full + 8 * ab);  // tile's accumulator complete
+        if (++ab == 2) {
+          ab = 0;
+          aph ^= 1u;
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // -------------------------------- converters --------------------------------
+    const int ct = threadIdx.x - 64;  // 0..127
+    int rs = 0, ss = 0;
+    uint32_t rph = 0, sph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        mbar_wait(raw_full + 8 * rs, rph);
+        mbar_wait(split_empty + 8 * ss, sph ^ 1u);
+        const float4* src = reinterpret_cast<const float4*>(sptr + (raw_s - base) + rs * kRawBytes);
+        float4* big = reinterpret_cast<float4*>(sptr + (split_s - base) + ss * kSplitBytes);
+        float4* sml = reinterpret_cast<float4*>(sptr + (split_s - base) + ss * kSplitBytes + kRawBytes);
+#pragma unroll 4
+        for (int i = ct; i < kRawBytes / 16; i += kConvThreads) {
+          const float4 x = src[i];
+          float4 hb, hs;
+          hb.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          hb.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          hb.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          hb.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          hs.x = x.x - hb.x;
+          hs.y = x.y - hb.y;
+          hs.z = x.z - hb.z;
+          hs.w = x.w - hb.w;
+          big[i] = hb;
+          sml[i] = hs;
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(raw_empty + 8 * rs);
+          mbar_arrive(split_full + 8 * ss);
+        }
+        if (++rs == kRawStages) {
+          rs = 0;
+          rph ^= 1u;
+        }
+        if (++ss == kSplitStages) {
+          ss = 0;
+          sph ^= 1u;
+        }
+      }
+    }
+  } else {
+    // --------------------------------- epilogue ---------------------------------
+    const int quad = warp & 3;  // TMEM lanes quad*32 .. +31 (tcgen05.ld lane restriction)
+    const int row_in_tile = quad * 32 + lane;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int64_t tm, tn;
+      tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+      mbar_wait(acc_full + 8 * ab, aph);
+      tc_fence_after();
+      const int64_t row = tm * kBM + row_in_tile;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols);
+#pragma unroll 1
+      for (int c = 0; c < kBN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c, r);
+        tmem_ld_wait();
+        const int64_t col = tn * kBN + c;
+        if (row < m) {
+          float* dst = C + row * p + col;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (col + 4 * q < p)
+              *reinterpret_cast<float4*>(dst + 4 * q) =
+                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                              __uint_as_float(r[4 * q + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + 8 * ab);
+      if (++ab == 2) {
+        ab = 0;
+        aph ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+TileConfig kK4Configs[] = {
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, kBN, kBK, kSplitStages, kThreads, 1, kSmem, 1.0},
+};
+
+}  // namespace
+
+int tf32_tile_configs(int kernel, const TileConfig** out) {
+  if (kernel == MOA_KERNEL_SGEMM_3XTF32) {
+    *out = kK4Configs;
+    return 1;
+  }
   *out = nullptr;
   return 0;
 }
-int launch_sgemm_3xtf32(const moa_plan_t&, int64_t, int64_t, int64_t, const float*, const float*, float*,
-                        cudaStream_t) {
-  set_error("3xTF32 kernel not built yet");
-  return MOA_ERR_INVALID_DTYPE;
+
+int launch_sgemm_3xtf32(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
+                        float* C, cudaStream_t stream) {
+  CUtensorMap ta, tb;
+  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, m, n, kBK, kBM) ||
+      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n, p, 32, kBK))
+    return MOA_ERR_CUDA;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(k_sgemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    return MOA_ERR_CUDA;
+  }
+  k_sgemm_3xtf32<<<plan.grid, kThreads, kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n,
+                                                         plan.raster_group);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_sgemm_3xtf32 launch: ") + cudaGetErrorString(e));
+    return MOA_ERR_CUDA;
+  }
+  return MOA_OK;
 }
+
 }  // namespace moa

@@ -99,3 +99,36 @@ def test_plan_fp32(cuda_device):
     moa = _moa()
     assert moa.plan(16384, 16384, 16384, moa.F32).kernel == "sgemm_ffma"
     assert moa.plan(100, 101, 102, moa.F32).kernel == "sgemm_generic"
+
+
+# ----------------------------------------------------------------- K4 3xTF32 --
+
+def test_3xtf32_tolerance_and_truth_error(cuda_device):
+    """<= 5e-3 relative Frobenius vs the literal oracle (north_star); the error vs the
+    fp64-accumulated truth is reported (printed) separately."""
+    moa = _moa()
+    assert moa.plan(1024, 1024, 1024, moa.F32_3XTF32).kernel == "sgemm_3xtf32"
+    for (m, n, p) in [(128, 32, 128), (129, 40, 132), (256, 256, 256), (300, 1000, 260), (1000, 4, 8)]:
+        A, B = _host(m, n, p, 11)
+        C = _run(A, B, cuda_device, precision="3xtf32")
+        err_lit = _relfro(C, O.ip(A, B, fused=False))
+        err_truth = _relfro(C, O.ip_f32_truth(A, B))
+        print(f"3xtf32 {m}x{n}x{p}: rel err vs literal ip.c {err_lit:.3e}, vs fp64 truth {err_truth:.3e}")
+        assert err_lit <= 5e-3, (m, n, p, err_lit)
+        assert err_truth <= 1e-5 * np.sqrt(n), (m, n, p, err_truth)  # 3xTF32 ~ fp32-level accuracy
+
+
+def test_3xtf32_integer_inputs_exact(cuda_device):
+    """Values in {-4..4} are exact in TF32 (small part 0) and every partial sum is an
+    integer < 2^24: the tensor-core result must equal the oracle bit for bit (P6)."""
+    for (m, n, p) in [(256, 256, 256), (130, 96, 260)]:
+        A, B = _host(m, n, p, 12, kind=I.INT)
+        assert np.array_equal(_run(A, B, cuda_device, precision="3xtf32"), O.ip(A, B, fused=False))
+
+
+def test_3xtf32_identity(cuda_device):
+    m, n, p = 256, 128, 384
+    A, _ = _host(m, n, p, 13)
+    # A•I = big*1 + small*1: big is exact in TF32, small keeps >= 11 of its <= 13 bits
+    C = _run(A, np.eye(n, dtype=np.float32), cuda_device, precision="3xtf32")
+    assert np.max(np.abs(C - A) / np.maximum(np.abs(A), 1e-30)) <= 2.0 ** -20
