@@ -73,6 +73,6 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t 
 // Host: 2-D row-major tensor map {cols (inner), rows}, box {box_cols, box_rows},
 // 128B swizzle, zero fill out of bounds. Returns false (and sets the error) on failure.
 bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, int64_t rows, int64_t cols,
-               int box_cols, int box_rows);
+               int box_cols, int box_rows, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);
 
 }  // namespace moa

@@ -95,6 +95,14 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
                             ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 
+#ifdef MOA_TF32_DEBUG
+__device__ float g_dbg[4096];
+__device__ uint32_t g_dbgu[64];
+#define DBG(i, v) g_dbg[i] = (v)
+#else
+#define DBG(i, v)
+#endif
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_3xtf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n,
@@ -129,6 +137,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sptr + (tmem_slot - base));
+#ifdef MOA_TF32_DEBUG
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    g_dbgu[0] = tmem; g_dbgu[1] = base; g_dbgu[2] = kIdesc;
+    g_dbgu[3] = (uint32_t)smem_desc(split_s, 16, 1024); g_dbgu[4] = (uint32_t)(smem_desc(split_s, 16, 1024) >> 32);
+  }
+#endif
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
@@ -185,6 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_tf32(d, dAb, dBs, kIdesc, 1u);
             mma_tf32(d, dAb, dBb, kIdesc, 1u);
           }
+#ifdef MOA_TF32_DEBUG
+          atomicAdd(&g_dbgu[10], 3u * (kBK / 8));
+#endif
           tc_commit(split_empty + 8 * st);  // slab consumed once these MMAs complete
           if (++st == kSplitStages) {
             st = 0;
@@ -224,6 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           hs.w = x.w - hb.w;
           big[i] = hb;
           sml[i] = hs;
+          if (blockIdx.x == 0 && kt == 0 && i < 64) {
+            DBG(4 * i, x.x); DBG(256 + 4 * i, hb.x); DBG(512 + 4 * i, hs.x);
+          }
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
@@ -259,6 +279,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[16];
         tmem_ld16(taddr + c, r);
         tmem_ld_wait();
+        if (blockIdx.x == 0 && t == 0 && c == 0) {
+          for (int q = 0; q < 16; ++q) DBG(1024 + row_in_tile * 16 + q, __uint_as_float(r[q]));
+#ifdef MOA_TF32_DEBUG
+          for (int cc = 0; cc < 256; cc += 16) {  // dump all allocated columns of this lane
+            uint32_t z[16];
+            tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + cc, z);
+            tmem_ld_wait();
+            if (row_in_tile == 0) for (int q = 0; q < 16; ++q) g_dbg[3072 + cc + q] = __uint_as_float(z[q]);
+          }
+          if (row_in_tile == 0) g_dbgu[11] += 1;
+#endif
+        }
         const int64_t col = tn * kBN + c;
         if (row < m) {
           float* dst = C + row * p + col;

@@ -126,6 +126,23 @@ def test_3xtf32_integer_inputs_exact(cuda_device):
         assert np.array_equal(_run(A, B, cuda_device, precision="3xtf32"), O.ip(A, B, fused=False))
 
 
+def test_3xtf32_each_tile_config(cuda_device):
+    import torch
+    moa = _moa()
+    m, n, p = 300, 200, 520
+    A, B = _host(m, n, p, 14)
+    ref = O.ip(A, B, fused=False)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    base = moa.plan(m, n, p, moa.F32_3XTF32)
+    for (bn, st) in [(256, 2), (128, 3)]:
+        pl = moa.Plan(**{**base.__dict__, "bn": bn, "stages": st})
+        out = torch.empty((m, p), dtype=torch.float32, device=cuda_device)
+        moa.gemm_with_plan(tA, tB, out, pl, precision="3xtf32")
+        torch.cuda.synchronize()
+        assert _relfro(out.cpu().numpy(), ref) <= 5e-3
+        assert _relfro(out.cpu().numpy(), O.ip_f32_truth(A, B)) <= 1e-5 * np.sqrt(n)
+
+
 def test_3xtf32_identity(cuda_device):
     m, n, p = 256, 128, 384
     A, _ = _host(m, n, p, 13)
