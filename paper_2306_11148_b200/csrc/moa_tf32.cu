@@ -2,24 +2,28 @@
 // cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM).
 //
 //   C[(i*p)+j] := sum_k A[(i*n)+k] * B[(k*p)+j]      (Eq. 3)
-//   computed as  Ab*Bb + Ab*Bs + As*Bb,  x = xb + xs,  xb = x & 0xFFFFE000 (exact
-//   in TF32), xs = x - xb (exact in fp32)  — north_star's "documented TF32/3xTF32
-//   tensor-core variant"; NOT exact (tolerance 5e-3, reported separately).
+//   computed as  Ab*Bb + Ab*Bs + As*Bb  with  x = xb + xs,  xb = x & 0xFFFFE000,
+//   xs = x - xb (exact in fp32) — north_star's "documented TF32/3xTF32 tensor-core
+//   variant"; NOT exact (tolerance 5e-3 vs ip.c, reported separately).
 //
-// Structure (persistent, one CTA per SM, 128 x 128 output tiles, k-slabs of 32):
-//   warp 0      TMA producer: A row segments (128 rows x 32 floats, K-major) and
-//               B row segments (32 k-rows x 32-float boxes, MN-major — B is used
-//               exactly as stored, row-major, never transposed: Fig. 1) into
-//               a raw ring.
-//   warps 2..5  converters: raw slab -> (big, small) slabs, same swizzled layout
-//               (the split is elementwise, so no index math), then
+// Measured on B200 (tools/probe/umma_probe.cu): the TF32 datapath TRUNCATES an fp32
+// operand to its top 19 bits, so the raw fp32 tile already IS the exact big part
+// xb. Only the small parts are materialised.
+//
+// Structure (persistent, one CTA per SM, BM x BN output tiles, k-slabs of 32):
+//   warp 0      TMA producer: A row segments (BM rows x 32 floats, K-major,
+//               SWIZZLE_128B) and B row segments (32 k-rows x 32-float boxes,
+//               MN-major, SWIZZLE_128B_ATOM_32B — the only MN-major layout the
+//               tensor core accepts for 32-bit operands). B is used exactly as it
+//               is stored, row-major, never transposed (Fig. 1).
+//   warps 2..5  converters: small = x - trunc19(x) for the whole slab (the split is
+//               elementwise, so the small slab has the raw slab's layout), then
 //               fence.proxy.async so the tensor core sees the generic writes.
 //   warp 1      TMEM allocator + MMA issuer (one thread): per k-step of 8,
-//               3 x tcgen05.mma (M=128, N=128, K=8) into a TMEM accumulator;
-//               tcgen05.commit frees the split slab / publishes the tile.
+//               3 x tcgen05.mma (M=128, N=BN, K=8) into a TMEM accumulator;
+//               tcgen05.commit frees the stage / publishes the finished tile.
 //   warps 6..9  epilogue: tcgen05.ld 32x32b -> registers -> global (row-major C).
-// Accumulators are double-buffered in TMEM (2 x 128 columns) so the epilogue of
-// tile t overlaps the MMAs of tile t+1.
+// Accumulators are double-buffered in TMEM (2 x BN columns).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -34,20 +38,27 @@ namespace moa {
 namespace {
 using namespace ptx;
 
-constexpr int kBM = 128, kBN = 128, kBK = 32;  // floats
-constexpr int kRowBytes = kBK * 4;              // 128
-constexpr int kABytes = kBM * kRowBytes;        // 16 KiB
-constexpr int kBBox = 32 * kRowBytes;           // 32 k-rows x 32 floats = 4 KiB
-constexpr int kBBytes = (kBN / 32) * kBBox;     // 16 KiB
-constexpr int kRawBytes = kABytes + kBBytes;    // 32 KiB
-constexpr int kSplitBytes = 2 * kRawBytes;      // big A, big B, small A, small B
-constexpr int kRawStages = 2, kSplitStages = 2;
-constexpr int kAccCols = kBN;                   // fp32 accumulator columns per buffer
-constexpr int kTmemCols = 2 * kAccCols;         // double buffered
+constexpr int kBM = 128, kBK = 32;           // floats
+constexpr int kRowBytes = kBK * 4;           // 128
+constexpr int kABytes = kBM * kRowBytes;     // 16 KiB
+constexpr int kBBox = 32 * kRowBytes;        // one B box: 32 k-rows x 32 floats = 4 KiB
 constexpr int kThreads = 10 * 32;
 constexpr int kConvThreads = 128;
-// barriers: raw_full/raw_empty[2], split_full/split_empty[2], acc_full/acc_empty[2]
-constexpr int kSmem = 1024 + kRawStages * kRawBytes + kSplitStages * kSplitBytes + 12 * 8 + 16;
+
+template <int BN, int STAGES>
+struct K4Traits {
+  static constexpr int kBBytes = (BN / 32) * kBBox;
+  static constexpr int kRawBytes = kABytes + kBBytes;
+  static constexpr int kStageBytes = 2 * kRawBytes;  // raw + small
+  static constexpr int kAccCols = BN;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmem = 1024 + STAGES * kStageBytes + (3 * STAGES + 4) * 8 + 16;
+  static_assert(kTmemCols <= 512, "TMEM has 512 columns");
+  // Instruction descriptor: D fp32 (c_format=1 @4), A,B tf32 (=2 @7, @10), A K-major
+  // (bit15=0), B MN-major (bit16=1), N>>3 @17, M>>4 @24.
+  static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                                     ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+};
 
 // ---------------------------- tcgen05 helpers ----------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
@@ -85,64 +96,52 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4 [16,30),
-// SBO>>4 [32,46), version=1 [46,48), layout SWIZZLE_128B = 2 at [61,64).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// SBO>>4 [32,46), version=1 [46,48), layout at [61,64): SWIZZLE_128B = 2,
+// SWIZZLE_128B_BASE32B = 1.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint64_t layout) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (layout << 61);
 }
-// Instruction descriptor: D fp32 (c_format=1 @4), A,B tf32 (=2 @7, @10), A K-major
-// (bit15=0), B MN-major (bit16=1), N>>3 @17, M>>4 @24.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                            ((uint32_t)(kBN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
 
-#ifdef MOA_TF32_DEBUG
-__device__ float g_dbg[4096];
-__device__ uint32_t g_dbgu[64];
-#define DBG(i, v) g_dbg[i] = (v)
-#else
-#define DBG(i, v)
-#endif
+__device__ __forceinline__ float tf32_small(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
 
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_3xtf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n,
                    int group) {
+  using Tr = K4Traits<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw0 = smem_u32(smem_raw);
   const uint32_t base = (raw0 + 1023u) & ~1023u;
   uint8_t* sptr = smem_raw + (base - raw0);
-  const uint32_t raw_s = base;                                   // raw ring
-  const uint32_t split_s = base + kRawStages * kRawBytes;        // split ring
-  const uint32_t bars = split_s + kSplitStages * kSplitBytes;
-  const uint32_t raw_full = bars, raw_empty = bars + 16, split_full = bars + 32, split_empty = bars + 48;
-  const uint32_t acc_full = bars + 64, acc_empty = bars + 80;
-  const uint32_t tmem_slot = bars + 96;
+  const uint32_t bars = base + STAGES * Tr::kStageBytes;
+  const uint32_t raw_full = bars, sml_full = bars + 8 * STAGES, empty = bars + 16 * STAGES;
+  const uint32_t acc_full = bars + 24 * STAGES, acc_empty = acc_full + 16;
+  const uint32_t tmem_slot = acc_empty + 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles = tiles_m * tiles_n;
   const int ktiles = (int)((n + kBK - 1) / kBK);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(raw_full + 8 * s, 1);
-      mbar_init(raw_empty + 8 * s, kConvThreads / 32);
-      mbar_init(split_full + 8 * s, kConvThreads / 32);
-      mbar_init(split_empty + 8 * s, 1);
+      mbar_init(sml_full + 8 * s, kConvThreads / 32);
+      mbar_init(empty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + 8 * s, 1);
       mbar_init(acc_empty + 8 * s, 4);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 1) tmem_alloc(tmem_slot, Tr::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sptr + (tmem_slot - base));
-#ifdef MOA_TF32_DEBUG
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    g_dbgu[0] = tmem; g_dbgu[1] = base; g_dbgu[2] = kIdesc;
-    g_dbgu[3] = (uint32_t)smem_desc(split_s, 16, 1024); g_dbgu[4] = (uint32_t)(smem_desc(split_s, 16, 1024) >> 32);
-  }
-#endif
 
   if (warp == 0) {
     // ------------------------------- TMA producer -------------------------------
@@ -155,15 +154,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t tm, tn;
         tile_coords(t, tiles_m, tiles_n, group, tm, tn);
         for (int kt = 0; kt < ktiles; ++kt) {
-          mbar_wait(raw_empty + 8 * st, ph ^ 1u);
+          mbar_wait(empty + 8 * st, ph ^ 1u);
           const uint32_t fb = raw_full + 8 * st;
-          mbar_arrive_expect_tx(fb, kRawBytes);
-          const uint32_t dst = raw_s + st * kRawBytes;
+          mbar_arrive_expect_tx(fb, Tr::kRawBytes);
+          const uint32_t dst = base + st * Tr::kStageBytes;
           tma_load_2d(dst, &tmA, fb, kt * kBK, (int)(tm * kBM));
 #pragma unroll
-          for (int b = 0; b < kBN / 32; ++b)
-            tma_load_2d(dst + kABytes + b * kBBox, &tmB, fb, (int)(tn * kBN) + 32 * b, kt * kBK);
-          if (++st == kRawStages) {
+          for (int b = 0; b < BN / 32; ++b)
+            tma_load_2d(dst + kABytes + b * kBBox, &tmB, fb, (int)(tn * BN) + 32 * b, kt * kBK);
+          if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
           }
@@ -180,30 +179,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         mbar_wait(acc_empty + 8 * ab, aph ^ 1u);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(ab * kAccCols);
+        const uint32_t d = tmem + (uint32_t)(ab * Tr::kAccCols);
         for (int kt = 0; kt < ktiles; ++kt) {
-          mbar_wait(split_full + 8 * st, ph);
+          mbar_wait(raw_full + 8 * st, ph);
+          mbar_wait(sml_full + 8 * st, ph);
           tc_fence_after();
-          const uint32_t s0 = split_s + st * kSplitBytes;
-          const uint32_t a_big = s0, b_big = s0 + kABytes, a_sml = s0 + kRawBytes, b_sml = s0 + kRawBytes + kABytes;
+          const uint32_t a_big = base + st * Tr::kStageBytes, b_big = a_big + kABytes;
+          const uint32_t a_sml = a_big + Tr::kRawBytes, b_sml = a_sml + kABytes;
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             // A: K-major, k-step of 8 floats = 32 B inside the 128 B swizzle row; SBO = 8 rows.
-            const uint64_t dAb = smem_desc(a_big + kk * 32, 16, 1024);
-            const uint64_t dAs = smem_desc(a_sml + kk * 32, 16, 1024);
-            // B: MN-major, k-step of 8 rows = 1024 B; LBO = next 32-column box, SBO = 8 rows.
-            const uint64_t dBb = smem_desc(b_big + kk * 1024, kBBox, 1024);
-            const uint64_t dBs = smem_desc(b_sml + kk * 1024, kBBox, 1024);
+            const uint64_t dAb = smem_desc(a_big + kk * 32, 16, 1024, 2);
+            const uint64_t dAs = smem_desc(a_sml + kk * 32, 16, 1024, 2);
+            // B: MN-major BASE32B, k-step of 8 rows = 1024 B; LBO = next 32-column box,
+            // SBO = next group of 4 k-rows.
+            const uint64_t dBb = smem_desc(b_big + kk * 1024, kBBox, 512, 1);
+            const uint64_t dBs = smem_desc(b_sml + kk * 1024, kBBox, 512, 1);
             const uint32_t acc0 = (kt > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(d, dAs, dBb, kIdesc, acc0);
-            mma_tf32(d, dAb, dBs, kIdesc, 1u);
-            mma_tf32(d, dAb, dBb, kIdesc, 1u);
+            mma_tf32(d, dAs, dBb, Tr::kIdesc, acc0);   // small terms first
+            mma_tf32(d, dAb, dBs, Tr::kIdesc, 1u);
+            mma_tf32(d, dAb, dBb, Tr::kIdesc, 1u);
           }
-#ifdef MOA_TF32_DEBUG
-          atomicAdd(&g_dbgu[10], 3u * (kBK / 8));
-#endif
-          tc_commit(split_empty + 8 * st);  // slab consumed once these MMAs complete
-          if (++st == kSplitStages) {
+          tc_commit(empty + 8 * st);  // raw + small slab free once these MMAs complete
+          if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
           }
@@ -218,46 +216,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 6) {
     // -------------------------------- converters --------------------------------
     const int ct = threadIdx.x - 64;  // 0..127
-    int rs = 0, ss = 0;
-    uint32_t rph = 0, sph = 0;
+    int st = 0;
+    uint32_t ph = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
       for (int kt = 0; kt < ktiles; ++kt) {
-        mbar_wait(raw_full + 8 * rs, rph);
-        mbar_wait(split_empty + 8 * ss, sph ^ 1u);
-        const float4* src = reinterpret_cast<const float4*>(sptr + (raw_s - base) + rs * kRawBytes);
-        float4* big = reinterpret_cast<float4*>(sptr + (split_s - base) + ss * kSplitBytes);
-        float4* sml = reinterpret_cast<float4*>(sptr + (split_s - base) + ss * kSplitBytes + kRawBytes);
+        mbar_wait(raw_full + 8 * st, ph);  // implies the stage's previous MMAs are done
+        const float4* src = reinterpret_cast<const float4*>(sptr + st * Tr::kStageBytes);
+        float4* sml = reinterpret_cast<float4*>(sptr + st * Tr::kStageBytes + Tr::kRawBytes);
 #pragma unroll 4
-        for (int i = ct; i < kRawBytes / 16; i += kConvThreads) {
+        for (int i = ct; i < Tr::kRawBytes / 16; i += kConvThreads) {
           const float4 x = src[i];
-          float4 hb, hs;
-          hb.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          hb.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          hb.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          hb.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-          hs.x = x.x - hb.x;
-          hs.y = x.y - hb.y;
-          hs.z = x.z - hb.z;
-          hs.w = x.w - hb.w;
-          big[i] = hb;
-          sml[i] = hs;
-          if (blockIdx.x == 0 && kt == 0 && i < 64) {
-            DBG(4 * i, x.x); DBG(256 + 4 * i, hb.x); DBG(512 + 4 * i, hs.x);
-          }
+          sml[i] = make_float4(tf32_small(x.x), tf32_small(x.y), tf32_small(x.z), tf32_small(x.w));
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(raw_empty + 8 * rs);
-          mbar_arrive(split_full + 8 * ss);
-        }
-        if (++rs == kRawStages) {
-          rs = 0;
-          rph ^= 1u;
-        }
-        if (++ss == kSplitStages) {
-          ss = 0;
-          sph ^= 1u;
+        if (lane == 0) mbar_arrive(sml_full + 8 * st);
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1u;
         }
       }
     }
@@ -273,25 +249,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(acc_full + 8 * ab, aph);
       tc_fence_after();
       const int64_t row = tm * kBM + row_in_tile;
-      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols);
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * Tr::kAccCols);
 #pragma unroll 1
-      for (int c = 0; c < kBN; c += 16) {
+      for (int c = 0; c < BN; c += 16) {
         uint32_t r[16];
         tmem_ld16(taddr + c, r);
         tmem_ld_wait();
-        if (blockIdx.x == 0 && t == 0 && c == 0) {
-          for (int q = 0; q < 16; ++q) DBG(1024 + row_in_tile * 16 + q, __uint_as_float(r[q]));
-#ifdef MOA_TF32_DEBUG
-          for (int cc = 0; cc < 256; cc += 16) {  // dump all allocated columns of this lane
-            uint32_t z[16];
-            tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + cc, z);
-            tmem_ld_wait();
-            if (row_in_tile == 0) for (int q = 0; q < 16; ++q) g_dbg[3072 + cc + q] = __uint_as_float(z[q]);
-          }
-          if (row_in_tile == 0) g_dbgu[11] += 1;
-#endif
-        }
-        const int64_t col = tn * kBN + c;
+        const int64_t col = tn * BN + c;
         if (row < m) {
           float* dst = C + row * p + col;
 #pragma unroll
@@ -315,20 +279,48 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    tmem_dealloc(tmem, Tr::kTmemCols);
   }
 }
 
 TileConfig kK4Configs[] = {
-    {MOA_KERNEL_SGEMM_3XTF32, kBM, kBN, kBK, kSplitStages, kThreads, 1, kSmem, 1.0},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 256, kBK, 2, kThreads, 1, K4Traits<256, 2>::kSmem, 1.0},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 128, kBK, 3, kThreads, 1, K4Traits<128, 3>::kSmem, 0.9},
 };
+
+template <int BN, int ST>
+int launch_k4(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B, float* C,
+              cudaStream_t stream) {
+  using Tr = K4Traits<BN, ST>;
+  CUtensorMap ta, tb;
+  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, m, n, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n, p, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return MOA_ERR_CUDA;
+  auto kern = k_sgemm_3xtf32<BN, ST>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    return MOA_ERR_CUDA;
+  }
+  kern<<<plan.grid, kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n, plan.raster_group);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_sgemm_3xtf32 launch: ") + cudaGetErrorString(e));
+    return MOA_ERR_CUDA;
+  }
+  return MOA_OK;
+}
 
 }  // namespace
 
 int tf32_tile_configs(int kernel, const TileConfig** out) {
   if (kernel == MOA_KERNEL_SGEMM_3XTF32) {
     *out = kK4Configs;
-    return 1;
+    return (int)(sizeof(kK4Configs) / sizeof(kK4Configs[0]));
   }
   *out = nullptr;
   return 0;
@@ -336,27 +328,10 @@ int tf32_tile_configs(int kernel, const TileConfig** out) {
 
 int launch_sgemm_3xtf32(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
                         float* C, cudaStream_t stream) {
-  CUtensorMap ta, tb;
-  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, m, n, kBK, kBM) ||
-      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n, p, 32, kBK))
-    return MOA_ERR_CUDA;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(k_sgemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  });
-  if (attr_err != cudaSuccess) {
-    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-    return MOA_ERR_CUDA;
-  }
-  k_sgemm_3xtf32<<<plan.grid, kThreads, kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n,
-                                                         plan.raster_group);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error(std::string("k_sgemm_3xtf32 launch: ") + cudaGetErrorString(e));
-    return MOA_ERR_CUDA;
-  }
-  return MOA_OK;
+  if (plan.bn == 256 && plan.stages == 2) return launch_k4<256, 2>(plan, m, n, p, A, B, C, stream);
+  if (plan.bn == 128 && plan.stages == 3) return launch_k4<128, 3>(plan, m, n, p, A, B, C, stream);
+  set_error("no compiled 3xTF32 instance for this plan");
+  return MOA_ERR_INVALID_SHAPE;
 }
 
 }  // namespace moa
