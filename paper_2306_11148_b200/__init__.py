@@ -240,18 +240,33 @@ def gemm_host(A_host, B_host, C_host, A_dev, B_dev, C_dev, *, precision: Optiona
 class Comm:
     """Library-owned NCCL communicator; the 128-byte id travels over torch.distributed."""
 
+    @staticmethod
+    def exchange_unique_id(group=None, make_id=None) -> bytes:
+        """Rank 0 makes the 128-byte NCCL unique id (moa_comm_get_unique_id) and every
+        rank receives it over torch.distributed (any backend, e.g. gloo)."""
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        blob = None
+        if rank == 0:
+            if make_id is None:
+                uid = ctypes.create_string_buffer(128)
+                _check(_moa_comm_get_unique_id(uid), "moa_comm_get_unique_id")
+                blob = bytes(uid.raw)
+            else:
+                blob = bytes(make_id())
+            if len(blob) != 128:
+                raise ValueError("unique id must be 128 bytes")
+        obj = [blob]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return obj[0]
+
     def __init__(self, group=None, device: Optional[int] = None):
         torch = _torch()
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = torch.cuda.current_device() if device is None else device
-        uid = ctypes.create_string_buffer(128)
-        if self.rank == 0:
-            _check(_moa_comm_get_unique_id(uid), "moa_comm_get_unique_id")
-        obj = [bytes(uid.raw) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        uid = ctypes.create_string_buffer(obj[0], 128)
+        uid = ctypes.create_string_buffer(Comm.exchange_unique_id(group), 128)
         h = _vp()
         _check(_moa_comm_init(self.world, self.rank, uid, self.device, ctypes.byref(h)), "moa_comm_init")
         self._h = h

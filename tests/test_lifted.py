@@ -1,0 +1,104 @@
+"""Row-lifted (multi-processor) path: Fig. 4 ip_rows.c.
+
+CPU (`-m "not gpu"`): world_size-2 gloo processes exercise the host logic of
+moa_gemm_lifted — the 128-byte id exchange (Comm.exchange_unique_id), the row
+partition from the C ABI (moa_lift_rows), the broadcast of B from rank 0, the
+per-rank compute of its rows (oracle here — no GPU) and the gather of C in
+partition order — and check the assembled C equals the single-process oracle
+bit for bit (lifting is a re-indexing).
+GPU: a 1-rank NCCL communicator drives the real moa_gemm_lifted (broadcast,
+lifted compute, gather) and must equal moa_gemm bit for bit.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, m, n, p, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_11148_b200 as moa
+        from inputs import inputs as I
+        from oracle import oracle as O
+        uid = moa.Comm.exchange_unique_id(make_id=lambda: bytes(range(128)))
+        assert uid == bytes(range(128))
+        row0, rows = moa.lift_rows(m, world, rank)
+        A_local = I.host_matrix(rows, n, 3, I.ID_A, row0=row0)
+        B = torch.from_numpy(I.host_matrix(n, p, 3, I.ID_B)) if rank == 0 else torch.zeros((n, p), dtype=torch.float64)
+        dist.broadcast(B, src=0)  # the lifted path's one exchange (reading R13)
+        C_local = torch.from_numpy(O.ip_rowblock(A_local, B.numpy(), fused=True))
+        counts = [moa.lift_rows(m, world, g)[1] for g in range(world)]
+        parts = [torch.zeros((c, p), dtype=torch.float64) for c in counts]
+        dist.all_gather(parts, C_local) if len(set(counts)) == 1 else _gather_uneven(parts, C_local, rank, world)
+        if rank == 0:
+            C = torch.cat(parts).numpy()
+            A = I.host_matrix(m, n, 3, I.ID_A)
+            q.put(bool(np.array_equal(C, O.ip(A, B.numpy(), fused=True))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _gather_uneven(parts, mine, rank, world):
+    for g in range(world):
+        buf = mine if g == rank else parts[g]
+        dist.broadcast(buf, src=g)
+        if g == rank:
+            parts[g].copy_(mine)
+
+
+@pytest.mark.parametrize("m", [64, 37])
+def test_lifted_host_logic_gloo_world2(m):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, m, 24, 40, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    ok = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert ok
+
+
+@pytest.mark.gpu
+def test_lifted_nccl_single_rank_equals_gemm(cuda_device):
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        for (m, n, p) in [(1000, 256, 300), (129, 64, 128)]:
+            A = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+            B = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+            I.device_fill(A, 5, I.ID_A)
+            I.device_fill(B, 5, I.ID_B)
+            ref = moa.gemm(A, B)
+            C_local = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+            C_full = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+            moa.gemm_lifted(m, A, B, C_local, comm, C_full=C_full)
+            torch.cuda.synchronize()
+            assert torch.equal(C_local, ref) and torch.equal(C_full, ref)
+    finally:
+        comm.close()
+        dist.destroy_process_group()
