@@ -1,0 +1,18 @@
+"""Small-shape runs of every kernel (K1 fp64 TMA, K2 generic, K3 FFMA, K3g, K4 3xTF32)
+for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2306_11148_b200 as moa
+from inputs import inputs as I
+from oracle import oracle as O
+ok = True
+for (m, n, p) in [(200, 96, 260), (130, 34, 66)]:
+    for dt, prec in [(np.float64, None), (np.float32, None), (np.float32, "3xtf32")]:
+        A = I.host_matrix(m, n, 2, I.ID_A, dtype=dt); B = I.host_matrix(n, p, 2, I.ID_B, dtype=dt)
+        C = moa.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), precision=prec)
+        torch.cuda.synchronize()
+        err = np.linalg.norm(C.cpu().numpy() - O.ip(A, B)) / np.linalg.norm(O.ip(A, B))
+        print(m, n, p, dt.__name__, prec, moa.plan(m, n, p, {np.float64: 0, np.float32: 1}[dt] if prec is None else 2).kernel, f"{err:.2e}")
+        ok &= err < 5e-3
+print("ALL OK" if ok else "MISMATCH")
