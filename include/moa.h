@@ -108,6 +108,21 @@ int moa_gemm(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void
 int moa_gemm_with_plan(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype,
                        const moa_plan_t* plan, void* stream);
 
+/* moa_gemm_acc — the σ-blocked form with leading dimensions: C (+)= A • B for
+ * row-major operands with row strides lda >= n, ldb >= p, ldc >= p (elements),
+ * e.g. a column slice A[:, k0:k1] (lda = full n) and the contiguous row panel
+ * B[k0:k1, :] (MoA order: one byte range).
+ *   accumulate == 0: C := A • B (as moa_gemm);
+ *   accumulate != 0: C := C + A • B, continuing every element's fma chain from the
+ *   C in memory in k order — so a sequence of k-panel calls over ascending
+ *   panels reproduces the one-call result bit for bit (f64, f32): "the sigma loop
+ *   is broken up creating the block. This necessitates another addition loop to
+ *   add up the blocks". (3xTF32: the prior C is added in the epilogue.)
+ * Validation as moa_gemm, plus MOA_ERR_INVALID_SHAPE for a leading dimension
+ * smaller than its row length; aliasing is checked on the strided byte spans. */
+int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                 int64_t ldc, int accumulate, int dtype, void* stream);
+
 /* moa_gemm_host — end-to-end call on HOST buffers: copies A_host and B_host into
  * the caller's device buffers A_dev/B_dev (cudaMemcpyAsync H2D), runs moa_gemm
  * into C_dev, copies C_dev back to C_host (D2H), then synchronises `stream`.
@@ -136,6 +151,21 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
  * ------------------------------------------------------------------------ */
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                     int dtype, void* stream, moa_comm_t comm);
+
+/* moa_gemm_lifted_ex — as moa_gemm_lifted with an explicit number of k-panels
+ * (0 = the static choice moa_lift_panels). With npanels > 1 the broadcast of B
+ * is pipelined: B's rows are split into npanels contiguous k-panels (each one
+ * byte range in MoA row-major order), broadcast one after the other on a
+ * library-owned side stream, and the rank's compute for panel j (moa_gemm_acc,
+ * accumulate for j > 0) waits only for panel j — the exchange overlaps the
+ * lifted compute. Results are bitwise identical to npanels = 1. 1 <= npanels <= 16. */
+int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
+                       int dtype, void* stream, moa_comm_t comm, int npanels);
+
+/* moa_lift_panels — static k-panel count for the lifted exchange: 1 when B does
+ * not travel (nranks == 1), else ceil(bytes(B) / 512 MiB) clamped to [1, 8] and
+ * to n/64. Pure function. */
+int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks);
 
 /* ------------------------------------------------------------------------
  * moa_psi — MoA psi on a row-major array (appendix; bracket bridge

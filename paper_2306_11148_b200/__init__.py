@@ -22,6 +22,7 @@ from typing import Optional, Sequence
 __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
+    "gemm_acc", "lift_panels",
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
@@ -59,6 +60,9 @@ _moa_gemm = _sig("moa_gemm", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_gemm_with_plan = _sig("moa_gemm_with_plan", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, ctypes.POINTER(_PlanT), _vp])
 _moa_gemm_host = _sig("moa_gemm_host", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp])
 _moa_gemm_lifted = _sig("moa_gemm_lifted", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
+_moa_gemm_lifted_ex = _sig("moa_gemm_lifted_ex", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
+_moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp])
+_moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
 _moa_psi = _sig("moa_psi", [_i32, ctypes.POINTER(_i64), _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                             ctypes.POINTER(_i64)])
 _moa_lift_rows = _sig("moa_lift_rows", [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)])
@@ -107,6 +111,11 @@ def lift_rows(m: int, nparts: int, part: int) -> tuple[int, int]:
     r0, r = _i64(), _i64()
     _check(_moa_lift_rows(m, nparts, part, ctypes.byref(r0), ctypes.byref(r)), "moa_lift_rows")
     return r0.value, r.value
+
+
+def lift_panels(n: int, p: int, dtype: int = F64, nranks: int = 1) -> int:
+    """Static k-panel count of the pipelined lifted exchange (moa_lift_panels)."""
+    return int(_moa_lift_panels(n, p, dtype, nranks))
 
 
 def select_block_paper(l1_budget_bytes: int, elem_bytes: int) -> int:
@@ -219,6 +228,25 @@ def gemm_with_plan(A, B, out, plan_: Plan, *, precision: Optional[str] = None, s
     return out
 
 
+def gemm_acc(A, B, C, accumulate: bool, *, precision: Optional[str] = None, stream=None):
+    """C (+)= A • B on row-major (possibly row-strided) CUDA views: A may be a column
+    slice A_full[:, k0:k1], B a row panel, C any row-major view (moa_gemm_acc)."""
+    for name, t in (("A", A), ("B", B), ("C", C)):
+        if t.dim() != 2 or not t.is_cuda or (t.numel() > 0 and t.stride(1) != 1):
+            raise ValueError(f"{name} must be a 2-D row-major CUDA view (unit column stride)")
+    m, n = A.shape
+    p = B.shape[1]
+    if B.shape[0] != n or tuple(C.shape) != (m, p):
+        raise ValueError("shape mismatch (Eq. 1, P:59-64)")
+    code = _dtype_code(A)
+    if precision == "3xtf32":
+        code = F32_3XTF32
+    _check(_moa_gemm_acc(m, n, p, A.data_ptr() or None, max(A.stride(0), 1), B.data_ptr() or None,
+                         max(B.stride(0), 1), C.data_ptr() or None, max(C.stride(0), 1), int(bool(accumulate)), code,
+                         _stream_ptr(stream)), "moa_gemm_acc")
+    return C
+
+
 def gemm_host(A_host, B_host, C_host, A_dev, B_dev, C_dev, *, precision: Optional[str] = None, stream=None):
     """End-to-end C-ABI call on host buffers (pinned torch CPU tensors): H2D, GEMM, D2H, sync."""
     m, n = A_host.shape
@@ -288,7 +316,7 @@ class Comm:
 
 
 def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precision: Optional[str] = None,
-                stream=None):
+                stream=None, npanels: int = 0):
     """Row-lifted C := A • B across the communicator (collective; see moa.h)."""
     n = B.shape[0]
     p = B.shape[1]
@@ -298,7 +326,7 @@ def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precisi
     for name, t in (("A_local", A_local), ("B", B), ("C_local", C_local), ("C_full", C_full)):
         if t is not None and (not t.is_cuda or not t.is_contiguous()):
             raise ValueError(f"{name} must be a contiguous CUDA tensor")
-    _check(_moa_gemm_lifted(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None, C_local.data_ptr() or None,
-                            None if C_full is None else (C_full.data_ptr() or None), code, _stream_ptr(stream),
-                            comm.handle), "moa_gemm_lifted")
+    _check(_moa_gemm_lifted_ex(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None,
+                               C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
+                               code, _stream_ptr(stream), comm.handle, npanels), "moa_gemm_lifted_ex")
     return C_local

@@ -132,14 +132,50 @@ __device__ __forceinline__ void mma_slab(Acc<NBOX>& c, const uint8_t* a_base, co
 
 // Write the warp's 32 x (16*NBOX) block of C. Lane holds, for atom a and box b,
 // row rho(g) and columns {2t, 2t+1} (pair 0) and {2t+8, 2t+9} (pair 1).
+// Accumulate mode ("the addition loop to add up the blocks", across
+// launches): start the chain from the C already in memory instead of +0. Because
+// DMMA continues an fma chain from its C operand, a sequence of k-panel launches
+// reproduces the single-launch result bit for bit. Same fragment map as store_acc.
+template <int NBOX, bool kVec>
+__device__ __forceinline__ void load_acc(Acc<NBOX>& c, const double* __restrict__ C, int64_t m, int64_t p,
+                                         int64_t ldc, int64_t row0, int64_t col0, const FragOffsets& f) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t r = row0 + a * 8 + f.rr;
+    const double* crow = C + r * ldc;
+#pragma unroll
+    for (int b = 0; b < NBOX; ++b) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t col = col0 + b * 16 + 2 * f.t + 8 * q;
+        double lo = 0.0, hi = 0.0;
+        if (r < m) {
+          if (kVec) {
+            if (col < p) {
+              const double2 v = *reinterpret_cast<const double2*>(crow + col);
+              lo = v.x;
+              hi = v.y;
+            }
+          } else {
+            if (col < p) lo = crow[col];
+            if (col + 1 < p) hi = crow[col + 1];
+          }
+        }
+        c.v[a][b][0][q] = lo;
+        c.v[a][b][1][q] = hi;
+      }
+    }
+  }
+}
+
 template <int NBOX, bool kVec>
 __device__ __forceinline__ void store_acc(const Acc<NBOX>& c, double* __restrict__ C, int64_t m, int64_t p,
-                                          int64_t row0, int64_t col0, const FragOffsets& f) {
+                                          int64_t ldc, int64_t row0, int64_t col0, const FragOffsets& f) {
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int64_t r = row0 + a * 8 + f.rr;
     if (r >= m) continue;
-    double* crow = C + r * p;
+    double* crow = C + r * ldc;
 #pragma unroll
     for (int b = 0; b < NBOX; ++b) {
 #pragma unroll
@@ -184,8 +220,8 @@ struct K1Traits {
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n,
-                int group) {
+                double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate,
+                int64_t tiles_m, int64_t tiles_n, int group) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -247,7 +283,10 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
-    acc_zero(acc);
+    if (accumulate)
+      load_acc<Tr::kNBox, true>(acc, C, m, p, ldc, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
+    else
+      acc_zero(acc);
     for (int kt = 0; kt < ktiles; ++kt) {
       mbar_wait(full0 + 8 * stage, phase);
       const uint8_t* sa = sptr + stage * Tr::kStageBytes;
@@ -259,7 +298,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
         phase ^= 1u;
       }
     }
-    store_acc<Tr::kNBox, true>(acc, C, m, p, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
+    store_acc<Tr::kNBox, true>(acc, C, m, p, ldc, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
   }
 }
 
@@ -267,7 +306,8 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
 template <int BM, int BN, int WARPS_M, int WARPS_N>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     k_dgemm_generic(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int64_t m,
-                    int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n, int group) {
+                    int64_t n, int64_t p, int64_t lda, int64_t ldb, int64_t ldc, int accumulate, int64_t tiles_m,
+                    int64_t tiles_n, int group) {
   constexpr int kNBox = BN / WARPS_N / 16;
   constexpr int kThreads = WARPS_M * WARPS_N * 32;
   __shared__ __align__(1024) uint8_t sm[(BM + BN) * kRowBytes];
@@ -284,40 +324,45 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const int64_t row0 = tm * BM, col0 = tn * BN;
-    acc_zero(acc);
+    if (accumulate)
+      load_acc<kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
+    else
+      acc_zero(acc);
     for (int64_t k0 = 0; k0 < n; k0 += kBK) {
       __syncthreads();
       for (int e = threadIdx.x; e < BM * kBK; e += kThreads) {  // A: row r, k
         const int r = e / kBK, k = e % kBK;
         const int64_t gi = row0 + r, gk = k0 + k;
-        const double v = (gi < m && gk < n) ? A[gi * n + gk] : 0.0;
+        const double v = (gi < m && gk < n) ? A[gi * lda + gk] : 0.0;
         sA[(r * kRowBytes + (((k >> 1) ^ (r & 7)) << 4) + ((k & 1) << 3)) / 8] = v;
       }
       for (int e = threadIdx.x; e < kBK * BN; e += kThreads) {  // B: k-row, col
         const int k = e / BN, c = e % BN;
         const int64_t gk = k0 + k, gj = col0 + c;
-        const double v = (gk < n && gj < p) ? B[gk * p + gj] : 0.0;
+        const double v = (gk < n && gj < p) ? B[gk * ldb + gj] : 0.0;
         const int box = c >> 4, cc = c & 15;
         sB[(box * kBoxBytes + k * kRowBytes + (((cc >> 1) ^ (k & 7)) << 4) + ((cc & 1) << 3)) / 8] = v;
       }
       __syncthreads();
       mma_slab(acc, sa + wm * 32 * kRowBytes, sb + wn * kNBox * kBoxBytes, f);
     }
-    store_acc<kNBox, false>(acc, C, m, p, row0 + wm * 32, col0 + wn * kNBox * 16, f);
+    store_acc<kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
   }
 }
 
 // ------------------------------ host helpers ---------------------------------
-bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
-  return encode_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, base, rows, cols, 16, box_rows);
+bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  return encode_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, base, rows, cols, 16, box_rows, CU_TENSOR_MAP_SWIZZLE_128B,
+                   ld);
 }
 
 template <int BM, int BN, int WM, int WN, int ST>
-int launch_k1(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A, const double* B, double* C,
-              cudaStream_t stream) {
+int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   using Tr = K1Traits<BM, BN, WM, WN, ST>;
   CUtensorMap ta, tb;
-  if (!encode_2d_f64(&ta, A, m, n, BM) || !encode_2d_f64(&tb, B, n, p, 16)) return MOA_ERR_CUDA;
+  const int64_t m = g.m, n = g.n, p = g.p;
+  if (!encode_2d_f64(&ta, g.A, m, n, g.lda, BM) || !encode_2d_f64(&tb, g.B, n, p, g.ldb, 16)) return MOA_ERR_CUDA;
+  double* C = (double*)g.C;
   auto kern = k_dgemm_tma<BM, BN, WM, WN, ST>;
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
@@ -328,8 +373,8 @@ int launch_k1(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const dou
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n,
-                                                       plan.raster_group);
+  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
+                                                       plan.tiles_n, plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -389,19 +434,18 @@ int dgemm_tile_configs(int kernel, const TileConfig** out) {
   return 0;
 }
 
-int launch_dgemm_tma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A, const double* B,
-                     double* C, cudaStream_t stream) {
-  if (plan.bm == 128 && plan.bn == 128 && plan.stages == 6) return launch_k1<128, 128, 4, 2, 6>(plan, m, n, p, A, B, C, stream);
-  if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 1, 4>(plan, m, n, p, A, B, C, stream);
-  if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 2, 4>(plan, m, n, p, A, B, C, stream);
+int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  if (plan.bm == 128 && plan.bn == 128 && plan.stages == 6) return launch_k1<128, 128, 4, 2, 6>(plan, g, stream);
+  if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 1, 4>(plan, g, stream);
+  if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 2, 4>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }
 
-int launch_dgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A,
-                         const double* B, double* C, cudaStream_t stream) {
-  k_dgemm_generic<64, 64, 2, 2><<<plan.grid, 128, 0, stream>>>(A, B, C, m, n, p, plan.tiles_m, plan.tiles_n,
-                                                             plan.raster_group);
+int launch_dgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  k_dgemm_generic<64, 64, 2, 2><<<plan.grid, 128, 0, stream>>>(
+      (const double*)g.A, (const double*)g.B, (double*)g.C, g.m, g.n, g.p, g.lda, g.ldb, g.ldc, g.accumulate,
+      plan.tiles_m, plan.tiles_n, plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_generic launch: ") + cudaGetErrorString(e));

@@ -17,11 +17,17 @@
 #include "moa.h"
 #include "moa_internal.h"
 
+// Library-owned communicator: the NCCL communicator plus a side stream and events
+// used to pipeline the broadcast of B's k-panels against the lifted compute.
+constexpr int kMaxPanels = 16;
 struct moa_comm_s {
   ncclComm_t nccl = nullptr;
   int nranks = 0;
   int rank = 0;
   int device = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_panel[kMaxPanels] = {};
 };
 
 namespace moa {
@@ -82,8 +88,16 @@ int get_device_shape(int device, DeviceShape* out) {
   return MOA_OK;
 }
 
-// Validation shared by moa_gemm / moa_gemm_lifted / moa_gemm_host (before any CUDA call).
-int validate(int64_t m, int64_t n, int64_t p, const void* A, const void* B, const void* C, int dtype) {
+// Byte span [lo, hi) of a rows x cols matrix with row stride ld (elements).
+void span(const void* base, int64_t rows, int64_t cols, int64_t ld, int es, uintptr_t* lo, uintptr_t* hi) {
+  *lo = (uintptr_t)base;
+  *hi = *lo + (uintptr_t)(rows > 0 && cols > 0 ? ((rows - 1) * ld + cols) * es : 0);
+}
+
+// Validation shared by every GEMM entry point (before any CUDA call). Row-major
+// operands with leading dimensions lda >= n, ldb >= p, ldc >= p (elements).
+int validate_g(const GemmArgs& g, int dtype) {
+  const int64_t m = g.m, n = g.n, p = g.p;
   if (m < 0 || n < 0 || p < 0) {
     set_error("negative extent");
     return MOA_ERR_INVALID_SHAPE;
@@ -93,40 +107,52 @@ int validate(int64_t m, int64_t n, int64_t p, const void* A, const void* B, cons
     set_error("unknown dtype");
     return MOA_ERR_INVALID_DTYPE;
   }
-  int64_t mn, np_, mp, t;
-  if (!mul_ok(m, n, &mn) || !mul_ok(n, p, &np_) || !mul_ok(m, p, &mp) || !mul_ok(mn, es, &t) ||
-      !mul_ok(np_, es, &t) || !mul_ok(mp, es, &t)) {
+  if (g.lda < (n > 1 ? n : 1) || g.ldb < (p > 1 ? p : 1) || g.ldc < (p > 1 ? p : 1)) {
+    set_error("leading dimension smaller than the row length");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t t;
+  if (!mul_ok(m, g.lda, &t) || !mul_ok(t, es, &t) || !mul_ok(n, g.ldb, &t) || !mul_ok(t, es, &t) ||
+      !mul_ok(m, g.ldc, &t) || !mul_ok(t, es, &t) || !mul_ok(m, p, &t) || !mul_ok(m, n, &t) || !mul_ok(n, p, &t)) {
     set_error("extent product overflows int64");
     return MOA_ERR_INVALID_SHAPE;
   }
-  if ((mn > 0 && !A) || (np_ > 0 && !B) || (mp > 0 && !C)) {
+  if ((m * n > 0 && !g.A) || (n * p > 0 && !g.B) || (m * p > 0 && !g.C)) {
     set_error("NULL pointer for a non-empty operand");
     return MOA_ERR_NULL_POINTER;
   }
   auto mis = [es](const void* q) { return q && (reinterpret_cast<uintptr_t>(q) % (uintptr_t)es) != 0; };
-  if (mis(A) || mis(B) || mis(C)) {
+  if (mis(g.A) || mis(g.B) || mis(g.C)) {
     set_error("pointer not aligned to the element size");
     return MOA_ERR_MISALIGNED;
   }
-  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
-    if (xb <= 0 || yb <= 0) return false;
-    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
-    return a0 < b1 && b0 < a1;
-  };
-  if (overlap(C, mp * es, A, mn * es) || overlap(C, mp * es, B, np_ * es)) {
+  uintptr_t a0, a1, b0, b1, c0, c1;
+  span(g.A, m, n, g.lda, es, &a0, &a1);
+  span(g.B, n, p, g.ldb, es, &b0, &b1);
+  span(g.C, m, p, g.ldc, es, &c0, &c1);
+  auto ov = [](uintptr_t x0, uintptr_t x1, uintptr_t y0, uintptr_t y1) { return x0 < x1 && y0 < y1 && x0 < y1 && y0 < x1; };
+  if (ov(c0, c1, a0, a1) || ov(c0, c1, b0, b1)) {
     set_error("C overlaps A or B (':=' needs a distinct output)");
     return MOA_ERR_ALIASING;
   }
   return MOA_OK;
 }
 
-// Is this call describable by the TMA kernels? (strides multiple of 16 B, bases
-// 16-B aligned, coordinates fit the tensor map's int32.)
-bool tma_eligible(int64_t m, int64_t n, int64_t p, const void* A, const void* B, const void* C, int es) {
+GemmArgs dense(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C) {
+  return GemmArgs{m, n, p, A, B, C, n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, 0};
+}
+
+int validate(int64_t m, int64_t n, int64_t p, const void* A, const void* B, const void* C, int dtype) {
+  return validate_g(dense(m, n, p, A, B, const_cast<void*>(C)), dtype);
+}
+
+// Is this call describable by the TMA kernels? (row strides multiple of 16 B,
+// bases 16-B aligned, coordinates fit the tensor map's int32.)
+bool tma_eligible(const GemmArgs& g, int es) {
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   const int per16 = 16 / es;
-  return (n % per16 == 0) && (p % per16 == 0) && al16(A) && al16(B) && al16(C) && m < INT32_MAX && n < INT32_MAX &&
-         p < INT32_MAX;
+  return (g.lda % per16 == 0) && (g.ldb % per16 == 0) && (g.ldc % per16 == 0) && (g.p % per16 == 0) &&
+         al16(g.A) && al16(g.B) && al16(g.C) && g.m < INT32_MAX && g.n < INT32_MAX && g.p < INT32_MAX;
 }
 
 // The static chooser: among the compiled tile configs of
@@ -213,26 +239,67 @@ int check_device(const DeviceShape& ds) {
   return MOA_OK;
 }
 
-int run_plan(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C,
-             int dtype, cudaStream_t s) {
+int run_plan(const moa_plan_t& plan, const GemmArgs& g, int dtype, cudaStream_t s) {
   switch (plan.kernel) {
     case MOA_KERNEL_NONE: return MOA_OK;
-    case MOA_KERNEL_ZERO_FILL: {
-      cudaError_t e = cudaMemsetAsync(C, 0, (size_t)(m * p * elem_size(dtype)), s);
-      return e == cudaSuccess ? MOA_OK : cuda_fail(e, "cudaMemsetAsync");
+    case MOA_KERNEL_ZERO_FILL: {  // empty sum: C := 0, or C := C + 0 (nothing) when accumulating
+      if (g.accumulate) return MOA_OK;
+      const size_t es = (size_t)elem_size(dtype);
+      cudaError_t e = cudaMemset2DAsync(g.C, (size_t)g.ldc * es, 0, (size_t)g.p * es, (size_t)g.m, s);
+      return e == cudaSuccess ? MOA_OK : cuda_fail(e, "cudaMemset2DAsync");
     }
-    case MOA_KERNEL_DGEMM_TMA:
-      return launch_dgemm_tma(plan, m, n, p, (const double*)A, (const double*)B, (double*)C, s);
-    case MOA_KERNEL_DGEMM_GENERIC:
-      return launch_dgemm_generic(plan, m, n, p, (const double*)A, (const double*)B, (double*)C, s);
-    case MOA_KERNEL_SGEMM_FFMA:
-      return launch_sgemm_ffma(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
-    case MOA_KERNEL_SGEMM_GENERIC:
-      return launch_sgemm_generic(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
-    case MOA_KERNEL_SGEMM_3XTF32:
-      return launch_sgemm_3xtf32(plan, m, n, p, (const float*)A, (const float*)B, (float*)C, s);
+    case MOA_KERNEL_DGEMM_TMA: return launch_dgemm_tma(plan, g, s);
+    case MOA_KERNEL_DGEMM_GENERIC: return launch_dgemm_generic(plan, g, s);
+    case MOA_KERNEL_SGEMM_FFMA: return launch_sgemm_ffma(plan, g, s);
+    case MOA_KERNEL_SGEMM_GENERIC: return launch_sgemm_generic(plan, g, s);
+    case MOA_KERNEL_SGEMM_3XTF32: return launch_sgemm_3xtf32(plan, g, s);
     default: set_error("bad plan kernel id"); return MOA_ERR_INVALID_SHAPE;
   }
+}
+
+// The common GEMM path: validate, plan (optionally honouring an explicit tile
+// choice), launch.
+int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t stream) {
+  int rc = validate_g(g, dtype);
+  if (rc) return rc;
+  DeviceShape ds;
+  if ((rc = get_device_shape(-1, &ds))) return rc;
+  if ((rc = check_device(ds))) return rc;
+  moa_plan_t pl;
+  if ((rc = plan_impl(g.m, g.n, g.p, dtype, ds, tma_eligible(g, elem_size(dtype)), &pl))) return rc;
+  if (plan && pl.kernel == plan->kernel) {
+    // honour an explicit tile choice (the block-size experiment) if it is a compiled config
+    const TileConfig* cfgs = nullptr;
+    int nc = (pl.kernel == MOA_KERNEL_DGEMM_TMA || pl.kernel == MOA_KERNEL_DGEMM_GENERIC)
+                 ? dgemm_tile_configs(pl.kernel, &cfgs)
+                 : sgemm_tile_configs(pl.kernel, &cfgs);
+    bool found = false;
+    for (int i = 0; i < nc && !found; ++i)
+      if (cfgs[i].bm == plan->bm && cfgs[i].bn == plan->bn && cfgs[i].stages == plan->stages) {
+        pl.bm = cfgs[i].bm;
+        pl.bn = cfgs[i].bn;
+        pl.stages = cfgs[i].stages;
+        pl.threads = cfgs[i].threads;
+        pl.ctas_per_sm = cfgs[i].ctas_per_sm;
+        pl.smem_bytes = cfgs[i].smem_bytes;
+        pl.tiles_m = (g.m + pl.bm - 1) / pl.bm;
+        pl.tiles_n = (g.p + pl.bn - 1) / pl.bn;
+        pl.tiles = pl.tiles_m * pl.tiles_n;
+        const int64_t slots = (int64_t)ds.sms * pl.ctas_per_sm;
+        pl.grid = (int32_t)(pl.tiles < slots ? pl.tiles : slots);
+        if (plan->grid > 0 && plan->grid < pl.grid) pl.grid = plan->grid;
+        if (plan->raster_group > 0) pl.raster_group = plan->raster_group;
+        found = true;
+      }
+    if (!found) {
+      set_error("requested tile configuration is not compiled");
+      return MOA_ERR_INVALID_SHAPE;
+    }
+  } else if (plan && pl.kernel != MOA_KERNEL_NONE && pl.kernel != MOA_KERNEL_ZERO_FILL) {
+    set_error("plan kernel does not match the kernel this call requires");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  return run_plan(pl, g, dtype, stream);
 }
 
 ncclDataType_t nccl_type(int dtype) { return dtype == MOA_F64 ? ncclFloat64 : ncclFloat32; }
@@ -365,51 +432,17 @@ int moa_plan(int64_t m, int64_t n, int64_t p, int dtype, int device, moa_plan_t*
 
 int moa_gemm_with_plan(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype,
                        const moa_plan_t* plan, void* stream) {
-  int rc = validate(m, n, p, A, B, C, dtype);
-  if (rc) return rc;
-  DeviceShape ds;
-  if ((rc = get_device_shape(-1, &ds))) return rc;
-  if ((rc = check_device(ds))) return rc;
-  const bool tma_ok = tma_eligible(m, n, p, A, B, C, elem_size(dtype));
-  moa_plan_t pl;
-  if ((rc = plan_impl(m, n, p, dtype, ds, tma_ok, &pl))) return rc;
-  if (plan && pl.kernel == plan->kernel) {
-    // honour an explicit tile choice (the block-size experiment) if it is a compiled config
-    const TileConfig* cfgs = nullptr;
-    int nc = (pl.kernel == MOA_KERNEL_DGEMM_TMA || pl.kernel == MOA_KERNEL_DGEMM_GENERIC)
-                 ? dgemm_tile_configs(pl.kernel, &cfgs)
-                 : sgemm_tile_configs(pl.kernel, &cfgs);
-    bool found = false;
-    for (int i = 0; i < nc; ++i)
-      if (cfgs[i].bm == plan->bm && cfgs[i].bn == plan->bn && cfgs[i].stages == plan->stages) {
-        pl.bm = cfgs[i].bm;
-        pl.bn = cfgs[i].bn;
-        pl.stages = cfgs[i].stages;
-        pl.threads = cfgs[i].threads;
-        pl.ctas_per_sm = cfgs[i].ctas_per_sm;
-        pl.smem_bytes = cfgs[i].smem_bytes;
-        pl.tiles_m = (m + pl.bm - 1) / pl.bm;
-        pl.tiles_n = (p + pl.bn - 1) / pl.bn;
-        pl.tiles = pl.tiles_m * pl.tiles_n;
-        const int64_t slots = (int64_t)ds.sms * pl.ctas_per_sm;
-        pl.grid = (int32_t)(pl.tiles < slots ? pl.tiles : slots);
-        if (plan->grid > 0 && plan->grid < pl.grid) pl.grid = plan->grid;
-        if (plan->raster_group > 0) pl.raster_group = plan->raster_group;
-        found = true;
-      }
-    if (!found) {
-      set_error("requested tile configuration is not compiled");
-      return MOA_ERR_INVALID_SHAPE;
-    }
-  } else if (plan) {
-    set_error("plan kernel does not match the kernel this call requires");
-    return MOA_ERR_INVALID_SHAPE;
-  }
-  return run_plan(pl, m, n, p, A, B, C, dtype, (cudaStream_t)stream);
+  return gemm_impl(dense(m, n, p, A, B, C), dtype, plan, (cudaStream_t)stream);
 }
 
 int moa_gemm(int64_t m, int64_t n, int64_t p, const void* A, const void* B, void* C, int dtype, void* stream) {
-  return moa_gemm_with_plan(m, n, p, A, B, C, dtype, nullptr, stream);
+  return gemm_impl(dense(m, n, p, A, B, C), dtype, nullptr, (cudaStream_t)stream);
+}
+
+int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                 int64_t ldc, int accumulate, int dtype, void* stream) {
+  return gemm_impl(GemmArgs{m, n, p, A, B, C, lda, ldb, ldc, accumulate ? 1 : 0}, dtype, nullptr,
+                   (cudaStream_t)stream);
 }
 
 int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
@@ -469,26 +502,62 @@ int moa_comm_init(int nranks, int rank, const unsigned char id[128], int device,
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
+  if ((e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming)) != cudaSuccess) {
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return cuda_fail(e, "side stream / event");
+  }
+  for (int i = 0; i < kMaxPanels; ++i)
+    if ((e = cudaEventCreateWithFlags(&c->ev_panel[i], cudaEventDisableTiming)) != cudaSuccess) {
+      ncclCommDestroy(c->nccl);
+      delete c;
+      return cuda_fail(e, "panel events");
+    }
   *comm = c;
   return MOA_OK;
 }
 
 int moa_comm_destroy(moa_comm_t comm) {
   if (!comm) return MOA_OK;
+  if (comm->side) cudaStreamSynchronize(comm->side);
+  for (int i = 0; i < kMaxPanels; ++i)
+    if (comm->ev_panel[i]) cudaEventDestroy(comm->ev_panel[i]);
+  if (comm->ev_start) cudaEventDestroy(comm->ev_start);
+  if (comm->side) cudaStreamDestroy(comm->side);
   ncclResult_t r = ncclCommDestroy(comm->nccl);
   delete comm;
   return r == ncclSuccess ? MOA_OK : nccl_fail(r, "ncclCommDestroy");
 }
 
-int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
-                    int dtype, void* stream, moa_comm_t comm) {
+int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks) {
+  // Static choice (no autotuning): pipeline only when B actually travels; aim for
+  // <= 512 MiB per panel (a panel's broadcast then hides behind the previous
+  // panel's compute), at most 8 panels (each extra panel re-reads/writes C once).
+  if (nranks <= 1 || n <= 0 || p <= 0) return 1;
+  const int64_t bytes = n * p * elem_size(dtype);
+  int64_t k = (bytes + (512ll << 20) - 1) / (512ll << 20);
+  if (k > 8) k = 8;
+  if (k > n / 64) k = n / 64;
+  return k < 1 ? 1 : (int)k;
+}
+
+int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
+                       int dtype, void* stream, moa_comm_t comm, int npanels) {
   if (!comm) {
     set_error("NULL communicator");
     return MOA_ERR_NULL_POINTER;
   }
+  if (m < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if (npanels < 0 || npanels > kMaxPanels) {
+    set_error("npanels out of range");
+    return MOA_ERR_INVALID_SHAPE;
+  }
   int64_t row0 = 0, rows = 0;
-  int rc = moa_lift_rows(m < 0 ? 0 : m, comm->nranks, comm->rank, &row0, &rows);
-  if (m < 0) rc = MOA_ERR_INVALID_SHAPE;
+  int rc = moa_lift_rows(m, comm->nranks, comm->rank, &row0, &rows);
   if (rc) return rc;
   if ((rc = validate(rows, n, p, A_local, B, C_local, dtype))) return rc;
   const int64_t es = elem_size(dtype);
@@ -508,18 +577,56 @@ int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* 
   }
   cudaStream_t s = (cudaStream_t)stream;
   const ncclDataType_t ty = nccl_type(dtype);
-  // (1) every processor needs all of B (ip_rows.c reads B[(sigma*sizer)+j] with no
-  //     processor index): in-place broadcast from rank 0 over NVLink.
-  if (n * p > 0 && comm->nranks > 1) {
-    ncclResult_t r = ncclBroadcast(B, B, (size_t)(n * p), ty, 0, comm->nccl, s);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B)");
+  cudaError_t e;
+  int K = npanels > 0 ? npanels : moa_lift_panels(n, p, dtype, comm->nranks);
+  if (n < K) K = n > 0 ? (int)n : 1;
+  // k-panel boundaries: multiples of 32 rows of B (TMA alignment of the A column
+  // slice), as equal as possible. Each panel of B is ONE contiguous byte range
+  // (rows k0..k1 of a row-major B — MoA order), so it is broadcast as is.
+  int64_t bnd[kMaxPanels + 1];
+  for (int j = 0; j <= K; ++j) {
+    int64_t b = (n * j / K) / 32 * 32;
+    bnd[j] = j == K ? n : b;
   }
-  // (2) the lifted compute: this rank's rows of C (Fig. 4, k = rank).
-  if ((rc = moa_gemm(rows, n, p, A_local, B, C_local, dtype, stream))) return rc;
+  if (K == 1 || comm->nranks == 1) {
+    // (1) every processor needs all of B (ip_rows.c reads B[(sigma*sizer)+j] with no
+    //     processor index): in-place broadcast from rank 0 over NVLink.
+    if (n * p > 0 && comm->nranks > 1) {
+      ncclResult_t r = ncclBroadcast(B, B, (size_t)(n * p), ty, 0, comm->nccl, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B)");
+    }
+  } else {
+    // Pipelined exchange (NEXT-1 step 1): broadcast the k-panels of B on the side
+    // stream, each followed by an event the compute stream waits on.
+    if ((e = cudaEventRecord(comm->ev_start, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(comm->side, comm->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    for (int j = 0; j < K; ++j) {
+      const int64_t k0 = bnd[j], k1 = bnd[j + 1];
+      if (k1 > k0) {
+        char* bp = (char*)B + k0 * p * es;
+        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((k1 - k0) * p), ty, 0, comm->nccl, comm->side);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B panel)");
+      }
+      if ((e = cudaEventRecord(comm->ev_panel[j], comm->side)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    }
+  }
+  // (2) the lifted compute: this rank's rows of C (Fig. 4, k = rank), panel by panel.
+  //     Panel j > 0 continues every element's fma chain from panel j-1's C, so the
+  //     result is bitwise the one-launch result ("the addition loop to add up the
+  //     blocks").
+  for (int j = 0; j < K; ++j) {
+    const int64_t k0 = bnd[j], k1 = bnd[j + 1];
+    if (K > 1 && comm->nranks > 1)
+      if ((e = cudaStreamWaitEvent(s, comm->ev_panel[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    if (k1 <= k0 && j > 0) continue;
+    GemmArgs g{rows, k1 - k0, p, (const char*)A_local + k0 * es, (const char*)B + k0 * p * es, C_local,
+               n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
+    if ((rc = gemm_impl(g, dtype, nullptr, s))) return rc;
+  }
   // (3) optional gather of C (reading R14).
   if (C_full && m * p > 0) {
     if (comm->nranks == 1) {
-      cudaError_t e = cudaMemcpyAsync(C_full, C_local, (size_t)(m * p * es), cudaMemcpyDeviceToDevice, s);
+      e = cudaMemcpyAsync(C_full, C_local, (size_t)(m * p * es), cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(C_full)");
     } else if (m % comm->nranks == 0) {
       ncclResult_t r = ncclAllGather(C_local, C_full, (size_t)(rows * p), ty, comm->nccl, s);
@@ -539,6 +646,11 @@ int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* 
     }
   }
   return MOA_OK;
+}
+
+int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
+                    int dtype, void* stream, moa_comm_t comm) {
+  return moa_gemm_lifted_ex(m, n, p, A_local, B, C_local, C_full, dtype, stream, comm, 0);
 }
 
 }  // extern "C"

@@ -24,18 +24,25 @@ struct DeviceShape {
 // Thread-local error detail for moa_last_error().
 void set_error(const std::string& s);
 
-// Kernel launchers (moa_dgemm.cu / moa_sgemm.cu). Arguments are validated by the
-// host layer; the plan is a valid output of plan_*(). Return a moa_status.
-int launch_dgemm_tma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A, const double* B,
-                     double* C, cudaStream_t stream);
-int launch_dgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const double* A,
-                         const double* B, double* C, cudaStream_t stream);
-int launch_sgemm_ffma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
-                      float* C, cudaStream_t stream);
-int launch_sgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A,
-                         const float* B, float* C, cudaStream_t stream);
-int launch_sgemm_3xtf32(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A,
-                        const float* B, float* C, cudaStream_t stream);
+// One GEMM call as the kernels see it: row-major operands with leading dimensions
+// (elements) lda >= n, ldb >= p, ldc >= p; accumulate != 0 continues the chain
+// from the C in memory (C := C + A•B, each element's fma chain extended in k order).
+struct GemmArgs {
+  int64_t m, n, p;
+  const void* A;
+  const void* B;
+  void* C;
+  int64_t lda, ldb, ldc;
+  int accumulate;
+};
+
+// Kernel launchers (moa_dgemm.cu / moa_sgemm.cu / moa_tf32.cu). Arguments are
+// validated by the host layer; the plan is a valid output of the chooser.
+int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
+int launch_dgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
+int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
+int launch_sgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
+int launch_sgemm_3xtf32(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
 
 // Static tile configurations compiled into the library (the chooser's candidates).
 struct TileConfig {

@@ -70,9 +70,10 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t 
 }  // namespace ptx
 #endif  // __CUDACC__
 
-// Host: 2-D row-major tensor map {cols (inner), rows}, box {box_cols, box_rows},
-// 128B swizzle, zero fill out of bounds. Returns false (and sets the error) on failure.
+// Host: 2-D row-major tensor map {cols (inner), rows} with row stride ld, box
+// {box_cols, box_rows}, the given swizzle, zero fill out of bounds. Returns false (and sets the error) on failure.
 bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, int64_t rows, int64_t cols,
-               int box_cols, int box_rows, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B);
+               int box_cols, int box_rows, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B,
+               int64_t ld = -1 /* row stride in elements; -1 = cols */);
 
 }  // namespace moa

@@ -86,14 +86,44 @@ __device__ __forceinline__ void ffma_slab(SAcc& c, const uint8_t* sA, const uint
   }
 }
 
+// Accumulate mode: continue each element's fma chain from the C in memory.
 template <bool kVec>
-__device__ __forceinline__ void sstore(const SAcc& c, float* __restrict__ C, int64_t m, int64_t p, int64_t row0,
-                                       int64_t col0, int ty, int tx) {
+__device__ __forceinline__ void sload(SAcc& c, const float* __restrict__ C, int64_t m, int64_t p, int64_t ldc,
+                                      int64_t row0, int64_t col0, int ty, int tx) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t row = row0 + ty * 8 + r;
+    const float* crow = C + row * ldc;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t col = col0 + h * 64 + tx * 4;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (row < m) {
+        if (kVec) {
+          if (col < p) {
+            const float4 x = *reinterpret_cast<const float4*>(crow + col);
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (col + e < p) v[e] = crow[col + e];
+        }
+      }
+      c.v[r][2 * h] = make_float2(v[0], v[1]);
+      c.v[r][2 * h + 1] = make_float2(v[2], v[3]);
+    }
+  }
+}
+
+template <bool kVec>
+__device__ __forceinline__ void sstore(const SAcc& c, float* __restrict__ C, int64_t m, int64_t p, int64_t ldc,
+                                       int64_t row0, int64_t col0, int ty, int tx) {
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int64_t row = row0 + ty * 8 + r;
     if (row >= m) continue;
-    float* crow = C + row * p;
+    float* crow = C + row * ldc;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t col = col0 + h * 64 + tx * 4;
@@ -124,7 +154,8 @@ struct K3Traits {
 template <int STAGES>
 __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
     k_sgemm_ffma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n, int group) {
+                 float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate, int64_t tiles_m,
+                 int64_t tiles_n, int group) {
   using Tr = K3Traits<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -181,7 +212,10 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
-    sacc_zero(acc);
+    if (accumulate)
+      sload<true>(acc, C, m, p, ldc, tm * Tr::BM, tn * Tr::BN, ty, tx);
+    else
+      sacc_zero(acc);
     for (int kt = 0; kt < ktiles; ++kt) {
       mbar_wait(full0 + 8 * stage, phase);
       const uint8_t* sa = sptr + stage * Tr::kStageBytes;
@@ -193,14 +227,15 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
         phase ^= 1u;
       }
     }
-    sstore<true>(acc, C, m, p, tm * Tr::BM, tn * Tr::BN, ty, tx);
+    sstore<true>(acc, C, m, p, ldc, tm * Tr::BM, tn * Tr::BN, ty, tx);
   }
 }
 
 // Generic: 256 threads, single stage, predicated scalar loads into the same layout.
 __global__ void __launch_bounds__(256)
     k_sgemm_generic(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C, int64_t m,
-                    int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n, int group) {
+                    int64_t n, int64_t p, int64_t lda, int64_t ldb, int64_t ldc, int accumulate, int64_t tiles_m,
+                    int64_t tiles_n, int group) {
   constexpr int BM = 128, BN = 128;
   __shared__ __align__(1024) uint8_t sm[BM * kRowB + kBKf * BN * 4];
   float* sA = reinterpret_cast<float*>(sm);
@@ -213,25 +248,28 @@ __global__ void __launch_bounds__(256)
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const int64_t row0 = tm * BM, col0 = tn * BN;
-    sacc_zero(acc);
+    if (accumulate)
+      sload<false>(acc, C, m, p, ldc, row0, col0, ty, tx);
+    else
+      sacc_zero(acc);
     for (int64_t k0 = 0; k0 < n; k0 += kBKf) {
       __syncthreads();
       for (int e = threadIdx.x; e < BM * kBKf; e += 256) {
         const int r = e / kBKf, k = e % kBKf;
         const int64_t gi = row0 + r, gk = k0 + k;
-        const float v = (gi < m && gk < n) ? A[gi * n + gk] : 0.f;
+        const float v = (gi < m && gk < n) ? A[gi * lda + gk] : 0.f;
         sA[(r * kRowB + (((k >> 2) ^ (r & 7)) << 4) + (k & 3) * 4) / 4] = v;
       }
       for (int e = threadIdx.x; e < kBKf * BN; e += 256) {
         const int k = e / BN, c = e % BN;
         const int64_t gk = k0 + k, gj = col0 + c;
-        const float v = (gk < n && gj < p) ? B[gk * p + gj] : 0.f;
+        const float v = (gk < n && gj < p) ? B[gk * ldb + gj] : 0.f;
         sB[((c >> 5) * kBoxBf + k * kRowB + ((((c & 31) >> 2) ^ (k & 7)) << 4) + (c & 3) * 4) / 4] = v;
       }
       __syncthreads();
       ffma_slab(acc, sm, sm + BM * kRowB, ty, tx);
     }
-    sstore<false>(acc, C, m, p, row0, col0, ty, tx);
+    sstore<false>(acc, C, m, p, ldc, row0, col0, ty, tx);
   }
 }
 
@@ -273,13 +311,14 @@ int sgemm_tile_configs(int kernel, const TileConfig** out) {
   return tf32_tile_configs(kernel, out);
 }
 
-int launch_sgemm_ffma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
-                      float* C, cudaStream_t stream) {
+int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   using Tr = K3Traits<6>;
   CUtensorMap ta, tb;
-  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, m, n, kBKf, Tr::BM) ||
-      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n, p, 32, kBKf))
+  const int64_t m = g.m, n = g.n, p = g.p;
+  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.A, m, n, kBKf, Tr::BM, CU_TENSOR_MAP_SWIZZLE_128B, g.lda) ||
+      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.B, n, p, 32, kBKf, CU_TENSOR_MAP_SWIZZLE_128B, g.ldb))
     return MOA_ERR_CUDA;
+  float* C = (float*)g.C;
   auto kern = k_sgemm_ffma<6>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -290,8 +329,8 @@ int launch_sgemm_ffma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, c
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n,
-                                                       plan.raster_group);
+  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
+                                                       plan.tiles_n, plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_ffma launch: ") + cudaGetErrorString(e));
@@ -300,9 +339,10 @@ int launch_sgemm_ffma(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, c
   return MOA_OK;
 }
 
-int launch_sgemm_generic(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
-                         float* C, cudaStream_t stream) {
-  k_sgemm_generic<<<plan.grid, 256, 0, stream>>>(A, B, C, m, n, p, plan.tiles_m, plan.tiles_n, plan.raster_group);
+int launch_sgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  k_sgemm_generic<<<plan.grid, 256, 0, stream>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.m, g.n, g.p,
+                                                 g.lda, g.ldb, g.ldc, g.accumulate, plan.tiles_m, plan.tiles_n,
+                                                 plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_generic launch: ") + cudaGetErrorString(e));

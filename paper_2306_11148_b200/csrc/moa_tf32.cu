@@ -110,8 +110,8 @@ __device__ __forceinline__ float tf32_small(float x) {
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_3xtf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t tiles_m, int64_t tiles_n,
-                   int group) {
+                   float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate,
+                   int64_t tiles_m, int64_t tiles_n, int group) {
   using Tr = K4Traits<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw0 = smem_u32(smem_raw);
@@ -257,13 +257,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int64_t col = tn * BN + c;
         if (row < m) {
-          float* dst = C + row * p + col;
+          float* dst = C + row * ldc + col;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (col + 4 * q < p)
-              *reinterpret_cast<float4*>(dst + 4 * q) =
-                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                              __uint_as_float(r[4 * q + 3]));
+            if (col + 4 * q < p) {
+              float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+              if (accumulate) {  // 3xTF32 is not exact anyway: add the prior C in the epilogue
+                const float4 o = *reinterpret_cast<const float4*>(dst + 4 * q);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(dst + 4 * q) = v;
+            }
         }
       }
       tc_fence_before();
@@ -289,13 +294,15 @@ TileConfig kK4Configs[] = {
 };
 
 template <int BN, int ST>
-int launch_k4(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B, float* C,
-              cudaStream_t stream) {
+int launch_k4(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   using Tr = K4Traits<BN, ST>;
   CUtensorMap ta, tb;
-  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, m, n, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n, p, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  const int64_t m = g.m, n = g.n, p = g.p;
+  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.A, m, n, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B, g.lda) ||
+      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.B, n, p, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                 g.ldb))
     return MOA_ERR_CUDA;
+  float* C = (float*)g.C;
   auto kern = k_sgemm_3xtf32<BN, ST>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -306,7 +313,8 @@ int launch_k4(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const flo
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  kern<<<plan.grid, kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, plan.tiles_m, plan.tiles_n, plan.raster_group);
+  kern<<<plan.grid, kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
+                                                   plan.tiles_n, plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_3xtf32 launch: ") + cudaGetErrorString(e));
@@ -326,10 +334,9 @@ int tf32_tile_configs(int kernel, const TileConfig** out) {
   return 0;
 }
 
-int launch_sgemm_3xtf32(const moa_plan_t& plan, int64_t m, int64_t n, int64_t p, const float* A, const float* B,
-                        float* C, cudaStream_t stream) {
-  if (plan.bn == 256 && plan.stages == 2) return launch_k4<256, 2>(plan, m, n, p, A, B, C, stream);
-  if (plan.bn == 128 && plan.stages == 3) return launch_k4<128, 3>(plan, m, n, p, A, B, C, stream);
+int launch_sgemm_3xtf32(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  if (plan.bn == 256 && plan.stages == 2) return launch_k4<256, 2>(plan, g, stream);
+  if (plan.bn == 128 && plan.stages == 3) return launch_k4<128, 3>(plan, g, stream);
   set_error("no compiled 3xTF32 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }

@@ -23,14 +23,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, int64_t rows, int64_t cols,
-               int box_cols, int box_rows, CUtensorMapSwizzle swizzle) {
+               int box_cols, int box_rows, CUtensorMapSwizzle swizzle, int64_t ld) {
   auto enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled entry point unavailable");
     return false;
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * (cuuint64_t)esize};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld < 0 ? cols : ld) * (cuuint64_t)esize};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

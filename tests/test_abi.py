@@ -101,3 +101,18 @@ def test_validation_before_any_cuda_call():
 def test_gemm_host_and_lifted_validate_first():
     assert moa._moa_gemm_host(-1, 1, 1, None, None, None, None, None, None, 0, None) == 1
     assert moa._moa_gemm_lifted(4, 4, 4, None, None, None, None, 0, None, None) == 3  # NULL comm
+
+
+def test_lift_panels_static_choice():
+    assert moa.lift_panels(1000, 1000, 0, 1) == 1                 # B does not travel
+    assert moa.lift_panels(32768, 32768, 0, 8) == 8               # 8 GiB of B -> 8 panels
+    assert moa.lift_panels(8192, 8192, 0, 8) == 1                 # 512 MiB -> 1
+    assert moa.lift_panels(16384, 16384, 0, 2) == 4               # 2 GiB -> 4
+    assert moa.lift_panels(100, 1 << 22, 0, 4) == 1               # n/64 clamp
+
+
+def test_gemm_acc_validation_without_gpu():
+    A, B, C = 0x10000, 0x200000, 0x4000000
+    assert moa._moa_gemm_acc(4, 8, 8, A, 7, B, 8, C, 8, 0, 0, None) == 1      # lda < n
+    assert moa._moa_gemm_acc(4, 8, 8, A, 8, B, 8, C, 7, 0, 0, None) == 1      # ldc < p
+    assert moa._moa_gemm_acc(4, 8, 8, A, 8, B, 8, A + 8 * 20, 8, 0, 0, None) == 4  # C inside A's span

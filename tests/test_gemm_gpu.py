@@ -243,3 +243,44 @@ def test_gemm_host_e2e(cuda_device):
     dC = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
     moa.gemm_host(hA, hB, hC, dA, dB, dC)
     assert _bits_equal(hC.numpy(), O.ip(A, B, fused=True))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_k_panel_chain_is_bitwise_one_launch(cuda_device, dtype):
+    """moa_gemm_acc: C := A[:, :k1] • B[:k1]; C += A[:, k1:] • B[k1:] ... reproduces the
+    one-launch C bit for bit — the blocked sigma loop with its 'addition loop'
+     across launches. Split points include ones that break 16-byte
+    alignment (generic kernel for that panel): same arithmetic, same bits."""
+    import torch
+    moa = _moa()
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    ndt = np.float64 if dtype == "f64" else np.float32
+    m, n, p = 300, 520, 264
+    A = I.host_matrix(m, n, 21, I.ID_A, dtype=ndt)
+    B = I.host_matrix(n, p, 21, I.ID_B, dtype=ndt)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    full = moa.gemm(tA, tB)
+    for cuts in ([0, 256, 520], [0, 32, 64, 320, 520], [0, 37, 300, 301, 520], [0, 520]):
+        C = torch.full((m, p), float("nan"), dtype=tdt, device=cuda_device)
+        for j in range(len(cuts) - 1):
+            k0, k1 = cuts[j], cuts[j + 1]
+            moa.gemm_acc(tA[:, k0:k1], tB[k0:k1], C, accumulate=j > 0)
+        torch.cuda.synchronize()
+        assert torch.equal(C, full), cuts
+    ref = O.ip(A, B, fused=True)
+    assert np.array_equal(full.cpu().numpy(), ref)
+
+
+def test_strided_output_and_validation(cuda_device):
+    import torch
+    moa = _moa()
+    m, n, p = 130, 64, 96
+    A, B = _host(m, n, p, 22)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    big = torch.full((m, p + 10), -1.0, dtype=torch.float64, device=cuda_device)
+    moa.gemm_acc(tA, tB, big[:, 2:2 + p], accumulate=False)
+    torch.cuda.synchronize()
+    assert _bits_equal(big[:, 2:2 + p].cpu().numpy(), O.ip(A, B, fused=True))
+    assert torch.all(big[:, :2] == -1) and torch.all(big[:, 2 + p:] == -1)
+    rc = moa._moa_gemm_acc(m, n, p, tA.data_ptr(), n - 1, tB.data_ptr(), p, big.data_ptr(), p + 10, 0, 0, None)
+    assert rc == 1  # lda < n

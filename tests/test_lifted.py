@@ -102,3 +102,32 @@ def test_lifted_nccl_single_rank_equals_gemm(cuda_device):
     finally:
         comm.close()
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_lifted_pipelined_panels_single_rank(cuda_device):
+    """NEXT-1 step 1: the k-panel pipelined exchange path (side stream, per-panel events,
+    accumulate launches) gives the one-launch bits. Exercised here with one rank and
+    explicit npanels (the broadcast itself is a no-op with one rank)."""
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        m, n, p = 700, 1000, 300
+        A = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+        B = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+        I.device_fill(A, 6, I.ID_A)
+        I.device_fill(B, 6, I.ID_B)
+        ref = moa.gemm(A, B)
+        for K in (1, 2, 3, 5, 16):
+            C = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+            moa.gemm_lifted(m, A, B, C, comm, npanels=K)
+            torch.cuda.synchronize()
+            assert torch.equal(C, ref), K
+    finally:
+        comm.close()
+        dist.destroy_process_group()
