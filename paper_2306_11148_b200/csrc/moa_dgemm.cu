@@ -148,18 +148,12 @@ __device__ __forceinline__ void load_acc(Acc<NBOX>& c, const double* __restrict_
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int64_t col = col0 + b * 16 + 2 * f.t + 8 * q;
+        // scalar loads straight into the two atoms' accumulators (a double2 load
+        // would pair registers of different DMMA operands and cost copies)
         double lo = 0.0, hi = 0.0;
         if (r < m) {
-          if (kVec) {
-            if (col < p) {
-              const double2 v = *reinterpret_cast<const double2*>(crow + col);
-              lo = v.x;
-              hi = v.y;
-            }
-          } else {
-            if (col < p) lo = crow[col];
-            if (col + 1 < p) hi = crow[col + 1];
-          }
+          if (col < p) lo = crow[col];
+          if (col + 1 < p) hi = crow[col + 1];
         }
         c.v[a][b][0][q] = lo;
         c.v[a][b][1][q] = hi;
@@ -202,7 +196,10 @@ __device__ __forceinline__ void store_acc(const Acc<NBOX>& c, double* __restrict
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct K1Traits {
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
-  static constexpr int kProducerWarps = kConsumerWarps >= 8 ? 4 : 1;
+  static constexpr int kNBoxW = BN / WARPS_N / 16;
+  // Only the 32x64 warp tile (64 accumulators) needs the producer's registers.
+  static constexpr int kProducerWarps = (kConsumerWarps >= 8 && kNBoxW == 4) ? 4 : 1;
+  static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : 2;  // 32x16 warp tiles fit 2 CTAs/SM (96 regs)
   static constexpr bool kSetMaxNReg = kProducerWarps == 4;
   static constexpr int kProducerRegs = 40;
   static constexpr int kConsumerRegs = 232;
@@ -217,10 +214,14 @@ struct K1Traits {
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads, 1)
+// ACC (compile time, so the plain path keeps ptxas's in-place accumulator
+// allocation: a runtime flag made it insert register copies around every DMMA,
+// -5.4% at N=16384): start each tile's chain from the C in memory.
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC>
+__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads,
+                                  K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate,
+                double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n, int group) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
-    if (accumulate)
+    if constexpr (ACC)
       load_acc<Tr::kNBox, true>(acc, C, m, p, ldc, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
     else
       acc_zero(acc);
@@ -363,18 +364,22 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   const int64_t m = g.m, n = g.n, p = g.p;
   if (!encode_2d_f64(&ta, g.A, m, n, g.lda, BM) || !encode_2d_f64(&tb, g.B, n, p, g.ldb, 16)) return MOA_ERR_CUDA;
   double* C = (double*)g.C;
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST>;
+  auto kern = g.accumulate ? k_dgemm_tma<BM, BN, WM, WN, ST, true> : k_dgemm_tma<BM, BN, WM, WN, ST, false>;
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+    attr_err = cudaFuncSetAttribute(k_dgemm_tma<BM, BN, WM, WN, ST, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(k_dgemm_tma<BM, BN, WM, WN, ST, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
-                                                       plan.tiles_n, plan.raster_group);
+  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
+                                                       plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -384,12 +389,15 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
 }
 
 // The chooser's candidate lifted blocks. ctas_per_sm is refined at first use
-// from the occupancy API (registers are what limit it; see K1Traits).
+// from the occupancy API (registers are what limit it; see K1Traits). eta is the
+// per-tile efficiency relative to 128x128, measured once at N=16384 where wave
+// quantisation vanishes (profiles/r01_configs.json block_sweep: 0.9815 / 0.9722 /
+// 0.9599 of peak) — a property of the tile config, not a per-shape tuning.
 TileConfig kK1Configs[] = {
     // kernel, bm, bn, bk, stages, threads, ctas/SM, smem, eta
     {MOA_KERNEL_DGEMM_TMA, 128, 128, 16, 6, K1Traits<128, 128, 4, 2, 6>::kThreads, 1, K1Traits<128, 128, 4, 2, 6>::kSmem, 1.00},
-    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 1, 4>::kThreads, 1, K1Traits<128, 64, 4, 1, 4>::kSmem, 0.97},
-    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 2, 4>::kThreads, 2, K1Traits<64, 64, 2, 2, 4>::kSmem, 0.93},
+    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 2, 4>::kThreads, 1, K1Traits<128, 64, 4, 2, 4>::kSmem, 0.99},
+    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 4, 4>::kThreads, 2, K1Traits<64, 64, 2, 4, 4>::kSmem, 0.978},
 };
 TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
@@ -398,7 +406,7 @@ TileConfig kK2Configs[] = {
 template <int BM, int BN, int WM, int WN, int ST>
 int k1_occupancy() {
   using Tr = K1Traits<BM, BN, WM, WN, ST>;
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Tr::kThreads, Tr::kSmem) != cudaSuccess) return 0;
@@ -408,7 +416,7 @@ int k1_occupancy() {
 void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
-    int o[3] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 1, 4>(), k1_occupancy<64, 64, 2, 2, 4>()};
+    int o[3] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>()};
     for (int i = 0; i < 3; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
@@ -436,8 +444,8 @@ int dgemm_tile_configs(int kernel, const TileConfig** out) {
 
 int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   if (plan.bm == 128 && plan.bn == 128 && plan.stages == 6) return launch_k1<128, 128, 4, 2, 6>(plan, g, stream);
-  if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 1, 4>(plan, g, stream);
-  if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 2, 4>(plan, g, stream);
+  if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 2, 4>(plan, g, stream);
+  if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 4, 4>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }

@@ -151,10 +151,11 @@ struct K3Traits {
   static constexpr int kSmem = 1024 + STAGES * kStageBytes + 2 * STAGES * 8;
 };
 
-template <int STAGES>
+// ACC is compile-time so the plain path keeps its register allocation.
+template <int STAGES, bool ACC>
 __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
     k_sgemm_ffma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate, int64_t tiles_m,
+                 float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int64_t tiles_m,
                  int64_t tiles_n, int group) {
   using Tr = K3Traits<STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
-    if (accumulate)
+    if constexpr (ACC)
       sload<true>(acc, C, m, p, ldc, tm * Tr::BM, tn * Tr::BN, ty, tx);
     else
       sacc_zero(acc);
@@ -284,7 +285,7 @@ void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
     int n = 0;
-    auto kern = k_sgemm_ffma<6>;
+    auto kern = k_sgemm_ffma<6, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K3Traits<6>::kSmem) == cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, K3Traits<6>::kThreads, K3Traits<6>::kSmem) ==
             cudaSuccess &&
@@ -319,18 +320,20 @@ int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t st
       !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.B, n, p, 32, kBKf, CU_TENSOR_MAP_SWIZZLE_128B, g.ldb))
     return MOA_ERR_CUDA;
   float* C = (float*)g.C;
-  auto kern = k_sgemm_ffma<6>;
+  auto kern = g.accumulate ? k_sgemm_ffma<6, true> : k_sgemm_ffma<6, false>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+    attr_err = cudaFuncSetAttribute(k_sgemm_ffma<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(k_sgemm_ffma<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
-                                                       plan.tiles_n, plan.raster_group);
+  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
+                                                       plan.raster_group);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_ffma launch: ") + cudaGetErrorString(e));
