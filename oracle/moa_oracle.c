@@ -218,3 +218,33 @@ void oracle_ip_f32_in_f64_acc(double* C, const float* A, const float* B, i64 siz
       for (i64 j = 0; j < sizer; j++)
         C[j + i * sizer] = C[j + i * sizer] + (double)A[(i * shr0) + sigma] * (double)B[(sigma * sizer) + j];
 }
+
+/* ---------------- ipophp siblings ----------------
+ * "scalar operations: Matrix Multiplication (MM), Hadamard Product (HP), and the
+ * Kronecker Product (KP) using one algorithm/circuit (ipophp)".
+ * Hadamard: rho A = rho B = <m,n>; C[(i*n)+j] = A[(i*n)+j] * B[(i*n)+j]
+ *   (pointwise scalar operation; indexing distributes over it).
+ * Kronecker: A<m,n>, B<p,q> -> C<m*p, n*q>, the outer product (rank 4,
+ *   <m,n,p,q>) with its two middle axes interchanged and ravelled row-major:
+ *   C[((i*p)+k)*(n*q) + (j*q)+l] = A[(i*n)+j] * B[(k*q)+l].
+ * One rounding per element (a single product): exact results are unique. */
+void oracle_hadamard_f64(double* C, const double* A, const double* B, i64 m, i64 n) {
+  for (i64 i = 0; i < m; i++)
+    for (i64 j = 0; j < n; j++) C[(i * n) + j] = A[(i * n) + j] * B[(i * n) + j];
+}
+void oracle_hadamard_f32(float* C, const float* A, const float* B, i64 m, i64 n) {
+  for (i64 i = 0; i < m; i++)
+    for (i64 j = 0; j < n; j++) C[(i * n) + j] = A[(i * n) + j] * B[(i * n) + j];
+}
+void oracle_kron_f64(double* C, const double* A, const double* B, i64 m, i64 n, i64 p, i64 q) {
+  for (i64 i = 0; i < m; i++)
+    for (i64 j = 0; j < n; j++)
+      for (i64 k = 0; k < p; k++)
+        for (i64 l = 0; l < q; l++) C[((i * p) + k) * (n * q) + (j * q) + l] = A[(i * n) + j] * B[(k * q) + l];
+}
+void oracle_kron_f32(float* C, const float* A, const float* B, i64 m, i64 n, i64 p, i64 q) {
+  for (i64 i = 0; i < m; i++)
+    for (i64 j = 0; j < n; j++)
+      for (i64 k = 0; k < p; k++)
+        for (i64 l = 0; l < q; l++) C[((i * p) + k) * (n * q) + (j * q) + l] = A[(i * n) + j] * B[(k * q) + l];
+}

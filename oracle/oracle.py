@@ -55,6 +55,11 @@ def _load():
         lib.oracle_ip_cols_unfused_f64.restype = ctypes.c_int
         lib.oracle_ip_f32_in_f64_acc.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64]
         lib.oracle_ip_f32_in_f64_acc.restype = None
+        for t in ("f64", "f32"):
+            getattr(lib, f"oracle_hadamard_{t}").argtypes = [_vp, _vp, _vp, _i64, _i64]
+            getattr(lib, f"oracle_hadamard_{t}").restype = None
+            getattr(lib, f"oracle_kron_{t}").argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, _i64]
+            getattr(lib, f"oracle_kron_{t}").restype = None
         _lib = lib
     return _lib
 
@@ -169,6 +174,27 @@ def ip_f32_truth(A: np.ndarray, B: np.ndarray) -> np.ndarray:
     p = B.shape[1]
     C = np.empty((m, p), dtype=np.float64)
     _load().oracle_ip_f32_in_f64_acc(_ptr(C), _ptr(A), _ptr(B), m, p, n)
+    return C
+
+
+def hadamard(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Hadamard product (pointwise ×)."""
+    if A.shape != B.shape or A.ndim != 2 or A.dtype != B.dtype:
+        raise ValueError("hadamard needs equal 2-D shapes and dtypes")
+    A, B = np.ascontiguousarray(A), np.ascontiguousarray(B)
+    C = np.empty_like(A)
+    getattr(_load(), f"oracle_hadamard_{_tag(A.dtype)}")(_ptr(C), _ptr(A), _ptr(B), A.shape[0], A.shape[1])
+    return C
+
+
+def kron(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Kronecker product via the outer-product definition."""
+    if A.ndim != 2 or B.ndim != 2 or A.dtype != B.dtype:
+        raise ValueError("kron needs 2-D operands of one dtype")
+    A, B = np.ascontiguousarray(A), np.ascontiguousarray(B)
+    (m, n), (p, q) = A.shape, B.shape
+    C = np.empty((m * p, n * q), dtype=A.dtype)
+    getattr(_load(), f"oracle_kron_{_tag(A.dtype)}")(_ptr(C), _ptr(A), _ptr(B), m, n, p, q)
     return C
 
 
