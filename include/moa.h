@@ -198,6 +198,21 @@ int moa_plan(int64_t m, int64_t n, int64_t p, int dtype, int device, moa_plan_t*
  * Errors: MOA_ERR_INVALID_SHAPE if even b = 1 does not fit. */
 int moa_select_block_paper(int64_t l1_budget_bytes, int elem_bytes, int64_t* b);
 
+/* ------------------------------------------------------------------------
+ * The "ipophp" siblings on the same row-major skeleton (P:372-378, P:515-530:
+ * "Matrix Multiplication (MM), Hadamard Product (HP), and the Kronecker Product
+ * (KP) using one algorithm/circuit"). dtype MOA_F64 or MOA_F32; device pointers,
+ * row-major contiguous; C must not overlap an input; asynchronous on `stream`.
+ * One rounding per element, so results equal the oracle bit for bit.
+ * moa_hadamard: rho A = rho B = rho C = <m,n>;  C[(i*n)+j] = A[(i*n)+j] * B[(i*n)+j].
+ * moa_kron:     A<m,n>, B<p,q>, C<m*p, n*q>;
+ *               C[((i*p)+k)*(n*q) + (j*q)+l] = A[(i*n)+j] * B[(k*q)+l]
+ *               (the outer product with its middle axes interchanged, ravelled).
+ * ------------------------------------------------------------------------ */
+int moa_hadamard(int64_t m, int64_t n, const void* A, const void* B, void* C, int dtype, void* stream);
+int moa_kron(int64_t m, int64_t n, int64_t p, int64_t q, const void* A, const void* B, void* C, int dtype,
+             void* stream);
+
 /* Communicator (library-owned; the 128-byte unique id is shipped by the caller,
  * e.g. over torch.distributed). `device` is the CUDA device the rank uses. */
 int moa_comm_get_unique_id(unsigned char id[128]);

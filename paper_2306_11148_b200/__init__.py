@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
-    "gemm_acc", "lift_panels",
+    "gemm_acc", "lift_panels", "hadamard", "kron",
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
@@ -63,6 +63,8 @@ _moa_gemm_lifted = _sig("moa_gemm_lifted", [_i64, _i64, _i64, _vp, _vp, _vp, _vp
 _moa_gemm_lifted_ex = _sig("moa_gemm_lifted_ex", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
 _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp])
 _moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
+_moa_hadamard = _sig("moa_hadamard", [_i64, _i64, _vp, _vp, _vp, _i32, _vp])
+_moa_kron = _sig("moa_kron", [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_psi = _sig("moa_psi", [_i32, ctypes.POINTER(_i64), _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                             ctypes.POINTER(_i64)])
 _moa_lift_rows = _sig("moa_lift_rows", [_i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)])
@@ -245,6 +247,36 @@ def gemm_acc(A, B, C, accumulate: bool, *, precision: Optional[str] = None, stre
                          max(B.stride(0), 1), C.data_ptr() or None, max(C.stride(0), 1), int(bool(accumulate)), code,
                          _stream_ptr(stream)), "moa_gemm_acc")
     return C
+
+
+def hadamard(A, B, out=None, *, stream=None):
+    """C = A ∘ B (pointwise ×) on the GPU (moa_hadamard)."""
+    torch = _torch()
+    if A.shape != B.shape or A.dim() != 2 or A.dtype != B.dtype:
+        raise ValueError("hadamard needs equal 2-D shapes and dtypes")
+    for t in (A, B, out):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("contiguous CUDA tensors expected")
+    out = torch.empty_like(A) if out is None else out
+    m, n = A.shape
+    _check(_moa_hadamard(m, n, A.data_ptr() or None, B.data_ptr() or None, out.data_ptr() or None, _dtype_code(A),
+                         _stream_ptr(stream)), "moa_hadamard")
+    return out
+
+
+def kron(A, B, out=None, *, stream=None):
+    """C = A ⊗ B (outer product + ravel) on the GPU (moa_kron)."""
+    torch = _torch()
+    if A.dim() != 2 or B.dim() != 2 or A.dtype != B.dtype:
+        raise ValueError("kron needs 2-D operands of one dtype")
+    for t in (A, B, out):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("contiguous CUDA tensors expected")
+    (m, n), (p, q) = A.shape, B.shape
+    out = torch.empty((m * p, n * q), dtype=A.dtype, device=A.device) if out is None else out
+    _check(_moa_kron(m, n, p, q, A.data_ptr() or None, B.data_ptr() or None, out.data_ptr() or None, _dtype_code(A),
+                     _stream_ptr(stream)), "moa_kron")
+    return out
 
 
 def gemm_host(A_host, B_host, C_host, A_dev, B_dev, C_dev, *, precision: Optional[str] = None, stream=None):

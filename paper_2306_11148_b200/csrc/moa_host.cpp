@@ -530,6 +530,65 @@ int moa_comm_destroy(moa_comm_t comm) {
   return r == ncclSuccess ? MOA_OK : nccl_fail(r, "ncclCommDestroy");
 }
 
+static int validate_elementwise(const void* A, int64_t na, const void* B, int64_t nb, const void* C, int64_t nc,
+                                int dtype) {
+  const int es = elem_size(dtype);
+  if (es == 0 || dtype == MOA_F32_3XTF32) {
+    set_error("dtype must be MOA_F64 or MOA_F32");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  if ((na > 0 && !A) || (nb > 0 && !B) || (nc > 0 && !C)) {
+    set_error("NULL pointer for a non-empty operand");
+    return MOA_ERR_NULL_POINTER;
+  }
+  auto mis = [es](const void* q) { return q && (reinterpret_cast<uintptr_t>(q) % (uintptr_t)es) != 0; };
+  if (mis(A) || mis(B) || mis(C)) {
+    set_error("pointer not aligned to the element size");
+    return MOA_ERR_MISALIGNED;
+  }
+  auto ov = [es](const void* x, int64_t xn, const void* y, int64_t yn) {
+    if (xn <= 0 || yn <= 0) return false;
+    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)(xn * es), b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)(yn * es);
+    return a0 < b1 && b0 < a1;
+  };
+  if (ov(C, nc, A, na) || ov(C, nc, B, nb)) {
+    set_error("C overlaps an input");
+    return MOA_ERR_ALIASING;
+  }
+  return MOA_OK;
+}
+
+int moa_hadamard(int64_t m, int64_t n, const void* A, const void* B, void* C, int dtype, void* stream) {
+  int64_t mn;
+  if (m < 0 || n < 0 || !mul_ok(m, n, &mn) || !mul_ok(mn, 8, &mn)) {
+    set_error("bad extents");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  mn = m * n;
+  int rc = validate_elementwise(A, mn, B, mn, C, mn, dtype);
+  if (rc) return rc;
+  if (mn == 0) return MOA_OK;
+  DeviceShape ds;
+  if ((rc = get_device_shape(-1, &ds)) || (rc = check_device(ds))) return rc;
+  return launch_hadamard(m, n, A, B, C, dtype, (cudaStream_t)stream);
+}
+
+int moa_kron(int64_t m, int64_t n, int64_t p, int64_t q, const void* A, const void* B, void* C, int dtype,
+             void* stream) {
+  int64_t mn, pq, out, t;
+  if (m < 0 || n < 0 || p < 0 || q < 0 || !mul_ok(m, n, &mn) || !mul_ok(p, q, &pq) || !mul_ok(mn, pq, &out) ||
+      !mul_ok(out, 8, &t)) {
+    set_error("bad extents");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int rc = validate_elementwise(A, mn, B, pq, C, out, dtype);
+  if (rc) return rc;
+  if (out == 0) return MOA_OK;
+  DeviceShape ds;
+  if ((rc = get_device_shape(-1, &ds)) || (rc = check_device(ds))) return rc;
+  return launch_kron(m, n, p, q, A, B, C, dtype, (cudaStream_t)stream);
+}
+
 int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks) {
   // Static choice (no autotuning): pipeline only when B actually travels; aim for
   // <= 512 MiB per panel (a panel's broadcast then hides behind the previous

@@ -44,6 +44,11 @@ int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t st
 int launch_sgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
 int launch_sgemm_3xtf32(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
 
+// ipophp siblings (moa_ipophp.cu); dense row-major operands, validated by the host.
+int launch_hadamard(int64_t m, int64_t n, const void* A, const void* B, void* C, int dtype, cudaStream_t s);
+int launch_kron(int64_t m, int64_t n, int64_t p, int64_t q, const void* A, const void* B, void* C, int dtype,
+                cudaStream_t s);
+
 // Static tile configurations compiled into the library (the chooser's candidates).
 struct TileConfig {
   int kernel;
