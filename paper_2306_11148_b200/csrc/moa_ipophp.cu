@@ -39,6 +39,8 @@ struct Vec<float> {
 __device__ __forceinline__ double2 pack(const double (&v)[2]) { return make_double2(v[0], v[1]); }
 __device__ __forceinline__ float4 pack(const float (&v)[4]) { return make_float4(v[0], v[1], v[2], v[3]); }
 __device__ __forceinline__ double2 vmul(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ double2 vscale(double a, double2 b) { return make_double2(a * b.x, a * b.y); }
+__device__ __forceinline__ float4 vscale(float a, float4 b) { return make_float4(a * b.x, a * b.y, a * b.z, a * b.w); }
 __device__ __forceinline__ float4 vmul(float4 a, float4 b) {
   return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
 }
@@ -82,6 +84,51 @@ __global__ void __launch_bounds__(256) k_hadamard_scalar(const T* __restrict__ A
 // r = i*p + k, column c = j*q + l. Vector path: the row length n*q is a multiple
 // of the vector width and C is aligned, so each thread stores kN consecutive
 // outputs (which may straddle two j's when q is small — handled per element).
+// Fast path (q % kN == 0, 16-B aligned B and C): every output vector lies inside
+// one j, so it is the scalar A[i][j] times one vector of the row B[k][:] — one
+// broadcast load, one vector load, one streaming store; 4 stores in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) k_kron_rowvec(const T* __restrict__ A, const T* __restrict__ B,
+                                                     T* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t q) {
+  using V = typename Vec<T>::V;
+  constexpr int kN = Vec<T>::kN;
+  constexpr int kU = 4;
+  const int64_t rows = m * p, vcols = n * q / kN, qv = q / kN;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t i = r / p, k = r - i * p;
+    const T* arow = A + i * n;
+    const V* brow = reinterpret_cast<const V*>(B + k * q);
+    V* crow = reinterpret_cast<V*>(C + r * n * q);
+    const int64_t step = blockDim.x;
+    const int64_t sj = step / qv, sl = step - sj * qv;
+    int64_t c = threadIdx.x, j = c / qv, l = c - j * qv;
+    for (; c + (kU - 1) * step < vcols; c += kU * step) {
+      V out[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        out[u] = vscale(__ldg(arow + j), __ldg(brow + l));
+        j += sj;
+        l += sl;
+        if (l >= qv) {
+          l -= qv;
+          ++j;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) __stcs(crow + c + u * step, out[u]);
+    }
+    for (; c < vcols; c += step) {
+      __stcs(crow + c, vscale(__ldg(arow + j), __ldg(brow + l)));
+      j += sj;
+      l += sl;
+      if (l >= qv) {
+        l -= qv;
+        ++j;
+      }
+    }
+  }
+}
+
 template <typename T, bool kVecStore>
 __global__ void __launch_bounds__(256) k_kron(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                                               int64_t m, int64_t n, int64_t p, int64_t q) {
@@ -94,18 +141,30 @@ __global__ void __launch_bounds__(256) k_kron(const T* __restrict__ A, const T* 
     const T* brow = B + k * q;
     T* crow = C + r * cols;
     if (kVecStore) {
-      for (int64_t c0 = (int64_t)threadIdx.x * kN; c0 < cols; c0 += (int64_t)blockDim.x * kN) {
+      // (j, l) of column c0 tracked incrementally: one division per row, none in the
+      // loop (64-bit division is emulated and was the bottleneck).
+      const int64_t step = (int64_t)blockDim.x * kN;
+      const int64_t sj = step / q, sl = step - sj * q;
+      int64_t c0 = (int64_t)threadIdx.x * kN;
+      int64_t j = c0 / q, l = c0 - j * q;
+      for (; c0 < cols; c0 += step) {
         T v[kN];
-        int64_t j = c0 / q, l = c0 - j * q;
+        int64_t jj = j, ll = l;
 #pragma unroll
         for (int e = 0; e < kN; ++e) {
-          v[e] = __ldg(arow + j) * __ldg(brow + l);
-          if (++l == q) {
-            l = 0;
-            ++j;
+          v[e] = __ldg(arow + jj) * __ldg(brow + ll);
+          if (++ll == q) {
+            ll = 0;
+            ++jj;
           }
         }
         __stcs(reinterpret_cast<V*>(crow + c0), pack(v));
+        j += sj;
+        l += sl;
+        if (l >= q) {
+          l -= q;
+          ++j;
+        }
       }
     } else {
       for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
@@ -157,7 +216,11 @@ int kron_t(int64_t m, int64_t n, int64_t p, int64_t q, const void* A, const void
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t blocks = rows < (int64_t)sms * 8 ? rows : (int64_t)sms * 8;
-  if (vec)
+  const bool rowvec = (q % Vec<T>::kN == 0) &&
+                      (((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15u) == 0);
+  if (rowvec)
+    k_kron_rowvec<T><<<(unsigned)blocks, 256, 0, s>>>((const T*)A, (const T*)B, (T*)C, m, n, p, q);
+  else if (vec)
     k_kron<T, true><<<(unsigned)blocks, 256, 0, s>>>((const T*)A, (const T*)B, (T*)C, m, n, p, q);
   else
     k_kron<T, false><<<(unsigned)blocks, 256, 0, s>>>((const T*)A, (const T*)B, (T*)C, m, n, p, q);

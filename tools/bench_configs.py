@@ -69,16 +69,63 @@ def rec(m, n, p, r, peak):
     return r
 
 
+HBM_GBS = 6535.7  # MEASURED_PEAKS.json hbm_gbs (copy, read+write)
+
+
+def ipophp(a, sampler):
+    """Hadamard and Kronecker (NEXT-4) against the HBM roofline: algorithmic bytes
+    (each input read once, output written once) / time."""
+    res = {}
+    N = 16384
+    A = torch.empty((N, N), dtype=torch.float64, device="cuda")
+    B = torch.empty_like(A)
+    C = torch.empty_like(A)
+    I.device_fill(A, 1, I.ID_A)
+    I.device_fill(B, 1, I.ID_B)
+    r = timed(lambda: moa.hadamard(A, B, out=C), a.window, sampler, 3 * 8 * N * N / 6e12)
+    byts = 3 * 8 * N * N
+    r.update({"shape": [N, N], "bytes": byts, "gbs": round(byts / (r["ms"] / 1e3) / 1e9, 1)})
+    r["frac_of_hbm"] = round(r["gbs"] / HBM_GBS, 4)
+    res["hadamard_f64_16384"] = r
+    del A, B
+    Ak = torch.empty((128, 128), dtype=torch.float64, device="cuda")
+    Bk = torch.empty((128, 128), dtype=torch.float64, device="cuda")
+    I.device_fill(Ak, 1, I.ID_A)
+    I.device_fill(Bk, 1, I.ID_B)
+    r = timed(lambda: moa.kron(Ak, Bk, out=C), a.window, sampler, 8 * N * N / 6e12)
+    byts = 8 * (N * N + 2 * 128 * 128)
+    r.update({"shape": "128x128 (x) 128x128 -> 16384x16384", "bytes": byts,
+              "gbs": round(byts / (r["ms"] / 1e3) / 1e9, 1)})
+    r["frac_of_hbm"] = round(r["gbs"] / HBM_GBS, 4)
+    res["kron_f64_128x128_128x128"] = r
+    # write-only ceiling reference on the same buffer (driver memset, not our kernel)
+    w = timed(lambda: C.zero_(), a.window, sampler, 8 * N * N / 6e12)
+    w_gbs = round(8 * N * N / (w["ms"] / 1e3) / 1e9, 1)
+    res["write_ceiling_memset_16384"] = {"ms": w["ms"], "gbs": w_gbs}
+    r["frac_of_write_ceiling"] = round(r["gbs"] / w_gbs, 4)
+    del C
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--window", type=float, default=1.0)
     ap.add_argument("--sizes", default="1024,1536,2048,3072,4096,6144,8192,16384")
     ap.add_argument("--skip-blocks", action="store_true")
+    ap.add_argument("--sections", default="c0,c1,c2,c3,ipophp")
     a = ap.parse_args()
+    secs = set(a.sections.split(","))
     sampler = ClockSampler(0, period=0.1)
     out = {"device": torch.cuda.get_device_name(0), "fp64_peak_tflops": FP64_DMMA_PEAK_TFLOPS,
            "ffma_peak_tflops": FFMA_PEAK_TFLOPS, "time": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
 
+    if "ipophp" in secs:
+        out["ipophp"] = ipophp(a, sampler)
+    if "c0" not in secs:
+        json.dump(out, sys.stdout, indent=1)
+        print()
+        return
     # configs[0]
     A, B, C = mats(256, 256, 256, torch.float64)
     r = timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, 5e-6)
