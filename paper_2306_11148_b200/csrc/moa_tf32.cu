@@ -288,9 +288,275 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------- K4 "TS" variant -------------------------------
+// Same pipeline, but both A parts live in TMEM: the converter warps read each raw A
+// row from shared memory into registers (the thread owns the row = its TMEM lane),
+// split it, and write big and small with tcgen05.st; the MMAs take A from TMEM
+// ([a_tmem]) and only B from shared memory. This removes every A operand read and
+// the A_small store from the shared-memory port, which the SS variant saturates.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int BN, int STAGES>
+struct K4TSTraits {
+  static constexpr int kBBytes = (BN / 32) * kBBox;
+  static constexpr int kRawBytes = kABytes + kBBytes;
+  static constexpr int kStageBytes = kRawBytes + kBBytes;  // raw A + raw B + small B
+  static constexpr int kAccBufs = (2 * BN + 64 * STAGES <= 512) ? 2 : 1;
+  static constexpr int kACol0 = kAccBufs * BN;              // A slots after the accumulators
+  static constexpr int kTmemCols = 512;
+  static constexpr int kSmem = 1024 + STAGES * kStageBytes + (3 * STAGES + 4) * 8 + 16;
+  static_assert(kAccBufs * BN + 64 * STAGES <= 512, "TMEM columns");
+  static constexpr uint32_t kIdesc = K4Traits<BN, STAGES>::kIdesc;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sgemm_3xtf32_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate,
+                      int64_t tiles_m, int64_t tiles_n, int group) {
+  using Tr = K4TSTraits<BN, STAGES>;
+  constexpr int NB = Tr::kAccBufs;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw0 = smem_u32(smem_raw);
+  const uint32_t base = (raw0 + 1023u) & ~1023u;
+  uint8_t* sptr = smem_raw + (base - raw0);
+  const uint32_t bars = base + STAGES * Tr::kStageBytes;
+  const uint32_t raw_full = bars, sml_full = bars + 8 * STAGES, empty = bars + 16 * STAGES;
+  const uint32_t acc_full = bars + 24 * STAGES, acc_empty = acc_full + 16;
+  const uint32_t tmem_slot = acc_empty + 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles = tiles_m * tiles_n;
+  const int ktiles = (int)((n + kBK - 1) / kBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(raw_full + 8 * s, 1);
+      mbar_init(sml_full + 8 * s, kConvThreads / 32);
+      mbar_init(empty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + 8 * s, 1);
+      mbar_init(acc_empty + 8 * s, 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Tr::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sptr + (tmem_slot - base));
+
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int64_t tm, tn;
+        tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          mbar_wait(empty + 8 * st, ph ^ 1u);
+          const uint32_t fb = raw_full + 8 * st;
+          mbar_arrive_expect_tx(fb, Tr::kRawBytes);
+          const uint32_t dst = base + st * Tr::kStageBytes;
+          tma_load_2d(dst, &tmA, fb, kt * kBK, (int)(tm * kBM));
+#pragma unroll
+          for (int b = 0; b < BN / 32; ++b)
+            tma_load_2d(dst + kABytes + b * kBBox, &tmB, fb, (int)(tn * BN) + 32 * b, kt * kBK);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(acc_empty + 8 * ab, aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(ab * BN);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          mbar_wait(raw_full + 8 * st, ph);
+          mbar_wait(sml_full + 8 * st, ph);
+          tc_fence_after();
+          const uint32_t b_big = base + st * Tr::kStageBytes + kABytes, b_sml = b_big + Tr::kBBytes;
+          const uint32_t a_big = tmem + (uint32_t)(Tr::kACol0 + 64 * st), a_sml = a_big + 32;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint64_t dBb = smem_desc(b_big + kk * 1024, kBBox, 512, 1);
+            const uint64_t dBs = smem_desc(b_sml + kk * 1024, kBBox, 512, 1);
+            const uint32_t acc0 = (kt > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_ts(d, a_sml + kk * 8, dBb, Tr::kIdesc, acc0);  // small terms first
+            mma_tf32_ts(d, a_big + kk * 8, dBs, Tr::kIdesc, 1u);
+            mma_tf32_ts(d, a_big + kk * 8, dBb, Tr::kIdesc, 1u);
+          }
+          tc_commit(empty + 8 * st);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+        tc_commit(acc_full + 8 * ab);
+        if (++ab == NB) {
+          ab = 0;
+          aph ^= 1u;
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // converters: thread = A row (its TMEM lane) for the A split; all 128 threads
+    // cooperatively split B into the small-B slab.
+    const int ct = threadIdx.x - 64;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        mbar_wait(raw_full + 8 * st, ph);  // implies the stage's previous MMAs are done
+        uint8_t* sa = sptr + st * Tr::kStageBytes;
+        uint32_t big[32], sml[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 16-B chunk c of the 128-B row (k = 4c..4c+3)
+          const float4 x = *reinterpret_cast<const float4*>(sa + row * kRowBytes + ((c ^ (row & 7)) << 4));
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t b = __float_as_uint(xs[e]) & 0xFFFFE000u;
+            big[4 * c + e] = b;
+            sml[4 * c + e] = __float_as_uint(xs[e] - __uint_as_float(b));
+          }
+        }
+        const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(Tr::kACol0 + 64 * st);
+        tmem_st32(ta, big);
+        tmem_st32(ta + 32, sml);
+        const float4* srcB = reinterpret_cast<const float4*>(sa + kABytes);
+        float4* smlB = reinterpret_cast<float4*>(sa + kABytes + Tr::kBBytes);
+#pragma unroll 4
+        for (int i = ct; i < Tr::kBBytes / 16; i += kConvThreads) {
+          const float4 x = srcB[i];
+          smlB[i] = make_float4(tf32_small(x.x), tf32_small(x.y), tf32_small(x.z), tf32_small(x.w));
+        }
+        tmem_st_wait();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sml_full + 8 * st);
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const int row_in_tile = quad * 32 + lane;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int64_t tm, tn;
+      tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+      mbar_wait(acc_full + 8 * ab, aph);
+      tc_fence_after();
+      const int64_t row = tm * kBM + row_in_tile;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c, r);
+        tmem_ld_wait();
+        const int64_t col = tn * BN + c;
+        if (row < m) {
+          float* dst = C + row * ldc + col;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (col + 4 * q < p) {
+              float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+              if (accumulate) {
+                const float4 o = *reinterpret_cast<const float4*>(dst + 4 * q);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(dst + 4 * q) = v;
+            }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + 8 * ab);
+      if (++ab == NB) {
+        ab = 0;
+        aph ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, Tr::kTmemCols);
+  }
+}
+
+template <int BN, int ST>
+int launch_k4ts(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  using Tr = K4TSTraits<BN, ST>;
+  CUtensorMap ta, tb;
+  const int64_t m = g.m, n = g.n, p = g.p;
+  if (!encode_2d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.A, m, n, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B, g.lda) ||
+      !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.B, n, p, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                 g.ldb))
+    return MOA_ERR_CUDA;
+  auto kern = k_sgemm_3xtf32_ts<BN, ST>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    return MOA_ERR_CUDA;
+  }
+  kern<<<plan.grid, kThreads, Tr::kSmem, stream>>>(ta, tb, (float*)g.C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
+                                                   plan.tiles_n, plan.raster_group);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_sgemm_3xtf32_ts launch: ") + cudaGetErrorString(e));
+    return MOA_ERR_CUDA;
+  }
+  return MOA_OK;
+}
+
+// (bn, stages): (256, 2) and (192, 3) are the TMEM-A ("TS") kernel, (128, 3) the
+// all-shared-memory ("SS") kernel, kept as the block-size-sweep reference.
 TileConfig kK4Configs[] = {
-    {MOA_KERNEL_SGEMM_3XTF32, kBM, 256, kBK, 2, kThreads, 1, K4Traits<256, 2>::kSmem, 1.0},
-    {MOA_KERNEL_SGEMM_3XTF32, kBM, 128, kBK, 3, kThreads, 1, K4Traits<128, 3>::kSmem, 0.9},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 256, kBK, 2, kThreads, 1, K4TSTraits<256, 2>::kSmem, 1.0},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 192, kBK, 3, kThreads, 1, K4TSTraits<192, 3>::kSmem, 0.98},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 128, kBK, 3, kThreads, 1, K4Traits<128, 3>::kSmem, 0.8},
 };
 
 template <int BN, int ST>
@@ -335,7 +601,8 @@ int tf32_tile_configs(int kernel, const TileConfig** out) {
 }
 
 int launch_sgemm_3xtf32(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
-  if (plan.bn == 256 && plan.stages == 2) return launch_k4<256, 2>(plan, g, stream);
+  if (plan.bn == 256 && plan.stages == 2) return launch_k4ts<256, 2>(plan, g, stream);
+  if (plan.bn == 192 && plan.stages == 3) return launch_k4ts<192, 3>(plan, g, stream);
   if (plan.bn == 128 && plan.stages == 3) return launch_k4<128, 3>(plan, g, stream);
   set_error("no compiled 3xTF32 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;

@@ -134,7 +134,7 @@ def test_3xtf32_each_tile_config(cuda_device):
     ref = O.ip(A, B, fused=False)
     tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
     base = moa.plan(m, n, p, moa.F32_3XTF32)
-    for (bn, st) in [(256, 2), (128, 3)]:
+    for (bn, st) in [(256, 2), (192, 3), (128, 3)]:
         pl = moa.Plan(**{**base.__dict__, "bn": bn, "stages": st})
         out = torch.empty((m, p), dtype=torch.float32, device=cuda_device)
         moa.gemm_with_plan(tA, tB, out, pl, precision="3xtf32")

@@ -122,19 +122,16 @@ def main():
 
     if "ipophp" in secs:
         out["ipophp"] = ipophp(a, sampler)
-    if "c0" not in secs:
-        json.dump(out, sys.stdout, indent=1)
-        print()
-        return
     # configs[0]
-    A, B, C = mats(256, 256, 256, torch.float64)
-    r = timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, 5e-6)
-    out["config0_fp64_256"] = rec(256, 256, 256, r, FP64_DMMA_PEAK_TFLOPS)
-    out["config0_fp64_256"]["plan"] = moa.plan(256, 256, 256).__dict__
+    if "c0" in secs:
+        A, B, C = mats(256, 256, 256, torch.float64)
+        r = timed(lambda: moa.gemm(A, B, out=C), a.window, sampler, 5e-6)
+        out["config0_fp64_256"] = rec(256, 256, 256, r, FP64_DMMA_PEAK_TFLOPS)
+        out["config0_fp64_256"]["plan"] = moa.plan(256, 256, 256).__dict__
 
     # configs[1] sweep + block-size experiment
     sweep = []
-    for N in [int(x) for x in a.sizes.split(",")]:
+    for N in ([int(x) for x in a.sizes.split(",")] if "c1" in secs else []):
         A, B, C = mats(N, N, N, torch.float64)
         est = 2.0 * N ** 3 / (FP64_DMMA_PEAK_TFLOPS * 0.9e12)
         pl = moa.plan(N, N, N)
@@ -165,6 +162,15 @@ def main():
         out["energy_exponent_fit_1024_8192"] = round(
             sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs), 3)
 
+    if "c2" in secs:
+        fp32_section(a, sampler, out)
+    if "c3" in secs:
+        skinny_section(a, sampler, out)
+    json.dump(out, sys.stdout, indent=1)
+    print()
+
+
+def fp32_section(a, sampler, out):
     # configs[2] fp32 N=16384
     N = 16384
     A, B, C = mats(N, N, N, torch.float32)
@@ -177,11 +183,24 @@ def main():
         r["kernel"] = moa.plan(N, N, N, moa.F32_3XTF32).kernel
         r["peak_note"] = "frac against TF32 nominal / 3 (three TF32 products per output term)"
         out["config2_fp32_16384_3xtf32"] = r
+        base = moa.plan(N, N, N, moa.F32_3XTF32)
+        blocks = []
+        for (bn, st) in [(256, 2), (192, 3), (128, 3)]:
+            q = moa.Plan(**{**base.__dict__, "bn": bn, "stages": st})
+            rb = rec(N, N, N, timed(lambda: moa.gemm_with_plan(A, B, C, q, precision="3xtf32"), a.window, sampler,
+                                    2.0 * N ** 3 / 200e12), TF32_NOMINAL_TFLOPS / 3)
+            rb.update({"bn": bn, "stages": st, "variant": "TS (A in TMEM)" if bn != 128 else "SS",
+                       "clocks": sampler.summary()})
+            sampler.samples = []
+            blocks.append(rb)
+        r["block_sweep"] = blocks
     except moa.MoAError as e:
         out["config2_fp32_16384_3xtf32"] = {"error": str(e)}
     del A, B, C
     torch.cuda.empty_cache()
 
+
+def skinny_section(a, sampler, out):
     # configs[3] skinny
     m, n, p = 65536, 512, 512
     A, B, C = mats(m, n, p, torch.float64)
@@ -191,8 +210,6 @@ def main():
     r["hbm_gbs_algorithmic"] = round(byts / (r["ms"] / 1e3) / 1e9, 1)
     r["plan"] = moa.plan(m, n, p).__dict__
     out["config3_fp64_65536x512x512"] = r
-    json.dump(out, sys.stdout, indent=1)
-    print()
 
 
 if __name__ == "__main__":
