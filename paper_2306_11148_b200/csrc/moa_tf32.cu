@@ -551,12 +551,15 @@ int launch_k4ts(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) 
   return MOA_OK;
 }
 
-// (bn, stages): (256, 2) and (192, 3) are the TMEM-A ("TS") kernel, (128, 3) the
-// all-shared-memory ("SS") kernel, kept as the block-size-sweep reference.
+// (bn, stages): (192, 3) and (256, 2) are the TMEM-A ("TS") kernel, (128, 3) the
+// all-shared-memory ("SS") kernel, kept as the block-size-sweep reference. eta =
+// per-tile efficiency measured once at N=16384 (profiles/r01_configs_fp32_ts.json:
+// 244.7 / 216.0 / 188.8 TF/s): 192 keeps double-buffered accumulators (2x192 + 2x64
+// A columns = 512) and a 3-stage ring; 256 fits only one accumulator and 2 stages.
 TileConfig kK4Configs[] = {
-    {MOA_KERNEL_SGEMM_3XTF32, kBM, 256, kBK, 2, kThreads, 1, K4TSTraits<256, 2>::kSmem, 1.0},
-    {MOA_KERNEL_SGEMM_3XTF32, kBM, 192, kBK, 3, kThreads, 1, K4TSTraits<192, 3>::kSmem, 0.98},
-    {MOA_KERNEL_SGEMM_3XTF32, kBM, 128, kBK, 3, kThreads, 1, K4Traits<128, 3>::kSmem, 0.8},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 192, kBK, 3, kThreads, 1, K4TSTraits<192, 3>::kSmem, 1.0},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 256, kBK, 2, kThreads, 1, K4TSTraits<256, 2>::kSmem, 0.88},
+    {MOA_KERNEL_SGEMM_3XTF32, kBM, 128, kBK, 3, kThreads, 1, K4Traits<128, 3>::kSmem, 0.77},
 };
 
 template <int BN, int ST>
