@@ -162,6 +162,22 @@ int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* 
 int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                        int dtype, void* stream, moa_comm_t comm, int npanels);
 
+/* moa_gemm_lifted_cols — dimension lifting of the COLUMNS (j axis) across ranks:
+ * Fig. 5 ip_cols.c at GPU level, "Dimension lifting over the columns of
+ * B reveals parallelism also". COLLECTIVE. Rank g owns columns
+ * [col0_g, col0_g + cols_g) = moa_lift_rows(p, G, g) of B and C.
+ *   A       : device, m x n on every rank; input on rank 0, overwritten with rank
+ *             0's A elsewhere (in-place broadcast: ip_cols.c reads A with no
+ *             column-group index).
+ *   B_local : device, n x cols_g, row-major contiguous (rank g's column block of B).
+ *   C_local : device, m x cols_g, receives rank g's column block of C.
+ *   C_full  : NULL, or device m x p receiving all of C on every rank; then
+ *   workspace must hold m * ceil(p / G) elements (not needed when G == 1).
+ * Bitwise identical to moa_gemm on one GPU (the k order of every element is
+ * unchanged by a j split). */
+int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,
+                         void* workspace, int dtype, void* stream, moa_comm_t comm);
+
 /* moa_lift_panels — static k-panel count for the lifted exchange: 1 when B does
  * not travel (nranks == 1), else ceil(bytes(B) / 512 MiB) clamped to [1, 8] and
  * to n/64. Pure function. */

@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
-    "gemm_acc", "lift_panels", "hadamard", "kron",
+    "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols",
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
@@ -63,6 +63,7 @@ _moa_gemm_lifted = _sig("moa_gemm_lifted", [_i64, _i64, _i64, _vp, _vp, _vp, _vp
 _moa_gemm_lifted_ex = _sig("moa_gemm_lifted_ex", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
 _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp])
 _moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
+_moa_gemm_lifted_cols = _sig("moa_gemm_lifted_cols", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_hadamard = _sig("moa_hadamard", [_i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_kron = _sig("moa_kron", [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_psi = _sig("moa_psi", [_i32, ctypes.POINTER(_i64), _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
@@ -361,4 +362,20 @@ def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precisi
     _check(_moa_gemm_lifted_ex(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None,
                                C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
                                code, _stream_ptr(stream), comm.handle, npanels), "moa_gemm_lifted_ex")
+    return C_local
+
+
+def gemm_lifted_cols(A, B_local, C_local, p: int, comm: Comm, C_full=None, workspace=None, *, stream=None):
+    """Column-lifted C := A • B across the communicator (collective; moa_gemm_lifted_cols).
+    Rank g passes its column block B_local (n x cols_g) and receives C_local (m x cols_g)."""
+    m, n = A.shape
+    code = _dtype_code(A)
+    for name, t in (("A", A), ("B_local", B_local), ("C_local", C_local), ("C_full", C_full),
+                    ("workspace", workspace)):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    _check(_moa_gemm_lifted_cols(m, n, p, A.data_ptr() or None, B_local.data_ptr() or None,
+                                 C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
+                                 None if workspace is None else (workspace.data_ptr() or None), code,
+                                 _stream_ptr(stream), comm.handle), "moa_gemm_lifted_cols")
     return C_local

@@ -707,6 +707,63 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
   return MOA_OK;
 }
 
+int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,
+                         void* workspace, int dtype, void* stream, moa_comm_t comm) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (p < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t col0 = 0, cols = 0;
+  int rc = moa_lift_rows(p, comm->nranks, comm->rank, &col0, &cols);  // the split of the j axis
+  if (rc) return rc;
+  if ((rc = validate(m, n, cols, A, B_local, C_local, dtype))) return rc;
+  const int64_t es = elem_size(dtype);
+  if (C_full && m * p > 0) {
+    if ((reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
+      set_error("C_full not aligned to the element size");
+      return MOA_ERR_MISALIGNED;
+    }
+    if (comm->nranks > 1 && !workspace) {
+      set_error("gathering column blocks needs a workspace of m * ceil(p / G) elements");
+      return MOA_ERR_NULL_POINTER;
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const ncclDataType_t ty = nccl_type(dtype);
+  // (1) every processor needs all of A (ip_cols.c reads A[(i*shr0)+sigma] with no
+  //     column-group index): in-place broadcast from rank 0.
+  if (m * n > 0 && comm->nranks > 1) {
+    ncclResult_t r = ncclBroadcast(A, A, (size_t)(m * n), ty, 0, comm->nccl, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(A)");
+  }
+  // (2) this rank's column block: C[:, col0:col0+cols] = A • B[:, col0:col0+cols].
+  if ((rc = moa_gemm(m, n, cols, A, B_local, C_local, dtype, stream))) return rc;
+  // (3) optional gather: rank r's block travels (broadcast) into the workspace, then
+  //     a strided 2-D copy places it at columns [col0_r, col0_r + cols_r) of C_full.
+  if (C_full && m * p > 0) {
+    for (int g = 0; g < comm->nranks; ++g) {
+      int64_t c0, cg;
+      moa_lift_rows(p, comm->nranks, g, &c0, &cg);
+      if (cg == 0) continue;
+      const void* src = C_local;
+      if (comm->nranks > 1) {
+        ncclResult_t r = ncclBroadcast(g == comm->rank ? C_local : nullptr, workspace, (size_t)(m * cg), ty, g,
+                                       comm->nccl, s);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(C column block)");
+        src = workspace;
+      }
+      cudaError_t e = cudaMemcpy2DAsync((char*)C_full + c0 * es, (size_t)(p * es), src, (size_t)(cg * es),
+                                        (size_t)(cg * es), (size_t)m, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_full)");
+    }
+  }
+  return MOA_OK;
+}
+
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                     int dtype, void* stream, moa_comm_t comm) {
   return moa_gemm_lifted_ex(m, n, p, A_local, B, C_local, C_full, dtype, stream, comm, 0);

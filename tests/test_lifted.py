@@ -131,3 +131,73 @@ def test_lifted_pipelined_panels_single_rank(cuda_device):
     finally:
         comm.close()
         dist.destroy_process_group()
+
+
+
+def _worker_cols(rank, world, port, m, n, p, q):
+    """Column lifting (Fig. 5 ip_cols.c across processes): rank g computes C[:, cols_g]
+    from all of A (broadcast) and its column block of B; the gathered C equals the
+    single-process oracle bit for bit."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_11148_b200 as moa
+        from inputs import inputs as I
+        from oracle import oracle as O
+        c0, cg = moa.lift_rows(p, world, rank)
+        A = torch.from_numpy(I.host_matrix(m, n, 4, I.ID_A)) if rank == 0 else torch.zeros((m, n), dtype=torch.float64)
+        dist.broadcast(A, src=0)
+        B = I.host_matrix(n, p, 4, I.ID_B)
+        C_local = torch.from_numpy(O.ip(A.numpy(), np.ascontiguousarray(B[:, c0:c0 + cg]), fused=True))
+        blocks = [torch.zeros((m, moa.lift_rows(p, world, g)[1]), dtype=torch.float64) for g in range(world)]
+        for g in range(world):
+            buf = C_local if g == rank else blocks[g]
+            dist.broadcast(buf, src=g)
+            if g == rank:
+                blocks[g].copy_(C_local)
+        if rank == 0:
+            C = torch.cat(blocks, dim=1).numpy()
+            q.put(bool(np.array_equal(C, O.ip(A.numpy(), B, fused=True))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_column_lifting_host_logic_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_cols, args=(r, 2, port, 20, 16, 37, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    ok = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert ok
+
+
+@pytest.mark.gpu
+def test_lifted_cols_nccl_single_rank(cuda_device):
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        m, n, p = 300, 128, 260
+        A = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+        B = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+        I.device_fill(A, 7, I.ID_A)
+        I.device_fill(B, 7, I.ID_B)
+        ref = moa.gemm(A, B)
+        C_local = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+        C_full = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+        moa.gemm_lifted_cols(A, B, C_local, p, comm, C_full=C_full)
+        torch.cuda.synchronize()
+        assert torch.equal(C_local, ref) and torch.equal(C_full, ref)
+    finally:
+        comm.close()
+        dist.destroy_process_group()
