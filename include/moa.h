@@ -124,11 +124,14 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
                  int64_t ldc, int accumulate, int dtype, void* stream);
 
 /* moa_gemm_host — end-to-end call on HOST buffers: copies A_host and B_host into
- * the caller's device buffers A_dev/B_dev (cudaMemcpyAsync H2D), runs moa_gemm
- * into C_dev, copies C_dev back to C_host (D2H), then synchronises `stream`.
- * Host buffers should be pinned for asynchronous copies. Same validation as
- * moa_gemm on the device buffers; host pointers must be non-NULL when their
- * extents are non-zero. */
+ * the caller's device buffers A_dev/B_dev, runs the GEMM into C_dev, copies C_dev
+ * back to C_host, and returns when C_host is complete (synchronous). Pipelined by
+ * row lifting: B goes first, then A in row panels on a library-owned
+ * copy stream; each panel's GEMM runs on `stream` as soon as its rows arrive and
+ * its C rows stream back on a second copy stream, so H2D, compute and D2H overlap.
+ * Bitwise identical to copy + moa_gemm + copy. Host buffers should be pinned.
+ * Same validation as moa_gemm on the device buffers; host pointers must be
+ * non-NULL when their extents are non-zero. */
 int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
                   void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream);
 

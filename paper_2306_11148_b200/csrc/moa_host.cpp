@@ -94,6 +94,40 @@ void span(const void* base, int64_t rows, int64_t cols, int64_t ld, int es, uint
   *hi = *lo + (uintptr_t)(rows > 0 && cols > 0 ? ((rows - 1) * ld + cols) * es : 0);
 }
 
+// Per-device resources of the pipelined host path (created once, owned by the
+// library): two copy streams and the events that chain panels across streams.
+constexpr int kMaxHostPanels = 32;
+struct HostPipe {
+  std::mutex mu;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev0 = nullptr;
+  cudaEvent_t evA[kMaxHostPanels] = {};
+  cudaEvent_t evC[kMaxHostPanels] = {};
+};
+std::mutex g_pipe_mu;
+std::map<int, HostPipe*> g_pipes;
+
+int host_pipe(int device, HostPipe** out) {
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  auto it = g_pipes.find(device);
+  if (it != g_pipes.end()) {
+    *out = it->second;
+    return MOA_OK;
+  }
+  auto* hp = new HostPipe;
+  cudaError_t e = cudaStreamCreateWithFlags(&hp->h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hp->d2h, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp->ev0, cudaEventDisableTiming);
+  for (int i = 0; i < kMaxHostPanels && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&hp->evA[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp->evC[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline streams/events");  // leaked on failure: process is broken
+  g_pipes[device] = hp;
+  *out = hp;
+  return MOA_OK;
+}
+
 // Validation shared by every GEMM entry point (before any CUDA call). Row-major
 // operands with leading dimensions lda >= n, ldb >= p, ldc >= p (elements).
 int validate_g(const GemmArgs& g, int dtype) {
@@ -456,13 +490,55 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   }
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  if (m * n > 0 && (e = cudaMemcpyAsync(A_dev, A_host, (size_t)(m * n * es), cudaMemcpyHostToDevice, s)) != cudaSuccess)
-    return cuda_fail(e, "H2D A");
-  if (n * p > 0 && (e = cudaMemcpyAsync(B_dev, B_host, (size_t)(n * p * es), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+  DeviceShape ds;
+  if ((rc = get_device_shape(-1, &ds))) return rc;
+  HostPipe* hp = nullptr;
+  if ((rc = host_pipe(ds.device, &hp))) return rc;
+  std::lock_guard<std::mutex> lk(hp->mu);
+  // Row lifting inside one GPU (rows of C depend only on the same rows of
+  // A, Fig. 1): A streams in row panels on a copy stream while earlier panels
+  // compute on `stream`, and each finished C panel streams back on a second copy
+  // stream. Panels are whole tile rows sized to ~7 waves of tiles each (static), so
+  // the panel GEMMs lose no wave efficiency; results are bitwise the one-call ones.
+  moa_plan_t pl;
+  if ((rc = moa_plan(m, n, p, dtype, ds.device, &pl))) return rc;
+  int64_t P = 1;
+  if (pl.kernel != MOA_KERNEL_NONE && pl.tiles > 0 && pl.bm > 0) {
+    P = pl.tiles / ((int64_t)ds.sms * 7);
+    if (P < 1) P = 1;
+    if (P > kMaxHostPanels) P = kMaxHostPanels;
+    if (P > pl.tiles_m) P = pl.tiles_m;
+  }
+  int64_t bnd[kMaxHostPanels + 1];
+  for (int64_t j = 0; j <= P; ++j) bnd[j] = j == P ? m : (pl.tiles_m * j / P) * (pl.bm > 0 ? pl.bm : 1);
+  if ((e = cudaEventRecord(hp->ev0, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  if ((e = cudaStreamWaitEvent(hp->h2d, hp->ev0, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+  if ((e = cudaStreamWaitEvent(hp->d2h, hp->ev0, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+  if (n * p > 0 && (e = cudaMemcpyAsync(B_dev, B_host, (size_t)(n * p * es), cudaMemcpyHostToDevice, hp->h2d)) !=
+                       cudaSuccess)
     return cuda_fail(e, "H2D B");
-  if ((rc = moa_gemm(m, n, p, A_dev, B_dev, C_dev, dtype, stream))) return rc;
-  if (m * p > 0 && (e = cudaMemcpyAsync(C_host, C_dev, (size_t)(m * p * es), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return cuda_fail(e, "D2H C");
+  for (int64_t j = 0; j < P; ++j) {
+    const int64_t r0 = bnd[j], rows = bnd[j + 1] - bnd[j];
+    if (rows * n > 0 &&
+        (e = cudaMemcpyAsync((char*)A_dev + r0 * n * es, (const char*)A_host + r0 * n * es, (size_t)(rows * n * es),
+                             cudaMemcpyHostToDevice, hp->h2d)) != cudaSuccess)
+      return cuda_fail(e, "H2D A panel");
+    if ((e = cudaEventRecord(hp->evA[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  }
+  for (int64_t j = 0; j < P; ++j) {
+    const int64_t r0 = bnd[j], rows = bnd[j + 1] - bnd[j];
+    if ((e = cudaStreamWaitEvent(s, hp->evA[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    if ((rc = moa_gemm(rows, n, p, (const char*)A_dev + r0 * n * es, B_dev, (char*)C_dev + r0 * p * es, dtype,
+                       stream)))
+      return rc;
+    if ((e = cudaEventRecord(hp->evC[j], s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(hp->d2h, hp->evC[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    if (rows * p > 0 &&
+        (e = cudaMemcpyAsync((char*)C_host + r0 * p * es, (const char*)C_dev + r0 * p * es, (size_t)(rows * p * es),
+                             cudaMemcpyDeviceToHost, hp->d2h)) != cudaSuccess)
+      return cuda_fail(e, "D2H C panel");
+  }
+  if ((e = cudaStreamSynchronize(hp->d2h)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(d2h)");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   return MOA_OK;
 }

@@ -229,11 +229,12 @@ def test_bench_configs_sampled_rows(cuda_device, cfg):
     assert _freivalds(C, tA, tB) <= 1e-12 * np.sqrt(n)
 
 
-def test_gemm_host_e2e(cuda_device):
-    """moa_gemm_host: host buffers in, host result out, same bits."""
+@pytest.mark.parametrize("shape", [(333, 128, 210), (4000, 256, 2048)])
+def test_gemm_host_e2e(cuda_device, shape):
+    """moa_gemm_host (row-panel pipelined H2D / compute / D2H): same bits as the oracle."""
     import torch
     moa = _moa()
-    m, n, p = 333, 128, 210
+    m, n, p = shape
     A, B = _host(m, n, p, 9)
     hA = torch.from_numpy(A).pin_memory()
     hB = torch.from_numpy(B).pin_memory()
