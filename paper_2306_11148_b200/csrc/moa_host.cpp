@@ -102,6 +102,7 @@ struct HostPipe {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t evA[kMaxHostPanels] = {};
+  cudaEvent_t evB[kMaxHostPanels] = {};
   cudaEvent_t evC[kMaxHostPanels] = {};
 };
 std::mutex g_pipe_mu;
@@ -120,6 +121,7 @@ int host_pipe(int device, HostPipe** out) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp->ev0, cudaEventDisableTiming);
   for (int i = 0; i < kMaxHostPanels && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&hp->evA[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp->evB[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp->evC[i], cudaEventDisableTiming);
   }
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline streams/events");  // leaked on failure: process is broken
@@ -511,28 +513,49 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   }
   int64_t bnd[kMaxHostPanels + 1];
   for (int64_t j = 0; j <= P; ++j) bnd[j] = j == P ? m : (pl.tiles_m * j / P) * (pl.bm > 0 ? pl.bm : 1);
+  // B itself is consumed in KB contiguous k-row panels by the FIRST row panel (an
+  // accumulate chain, bitwise the one-call result), so its transfer overlaps compute
+  // too; later row panels run after all of B has landed.
+  int64_t KB = (P > 1 && n >= 256) ? 4 : 1;
+  int64_t kb[kMaxHostPanels + 1];
+  for (int64_t j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
   if ((e = cudaEventRecord(hp->ev0, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   if ((e = cudaStreamWaitEvent(hp->h2d, hp->ev0, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
   if ((e = cudaStreamWaitEvent(hp->d2h, hp->ev0, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
-  if (n * p > 0 && (e = cudaMemcpyAsync(B_dev, B_host, (size_t)(n * p * es), cudaMemcpyHostToDevice, hp->h2d)) !=
-                       cudaSuccess)
-    return cuda_fail(e, "H2D B");
-  for (int64_t j = 0; j < P; ++j) {
-    const int64_t r0 = bnd[j], rows = bnd[j + 1] - bnd[j];
-    if (rows * n > 0 &&
-        (e = cudaMemcpyAsync((char*)A_dev + r0 * n * es, (const char*)A_host + r0 * n * es, (size_t)(rows * n * es),
-                             cudaMemcpyHostToDevice, hp->h2d)) != cudaSuccess)
-      return cuda_fail(e, "H2D A panel");
-    if ((e = cudaEventRecord(hp->evA[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  auto h2d_rows = [&](const void* hsrc, void* ddst, int64_t r0, int64_t rows, int64_t rowlen) -> cudaError_t {
+    if (rows * rowlen <= 0) return cudaSuccess;
+    return cudaMemcpyAsync((char*)ddst + r0 * rowlen * es, (const char*)hsrc + r0 * rowlen * es,
+                           (size_t)(rows * rowlen * es), cudaMemcpyHostToDevice, hp->h2d);
+  };
+  // copy order on the H2D engine: A panel 0, B k-panels, A panels 1..P-1
+  if ((e = h2d_rows(A_host, A_dev, bnd[0], bnd[1] - bnd[0], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
+  if ((e = cudaEventRecord(hp->evA[0], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  for (int64_t j = 0; j < KB; ++j) {
+    if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
+    if ((e = cudaEventRecord(hp->evB[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   }
-  for (int64_t j = 0; j < P; ++j) {
-    const int64_t r0 = bnd[j], rows = bnd[j + 1] - bnd[j];
-    if ((e = cudaStreamWaitEvent(s, hp->evA[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
-    if ((rc = moa_gemm(rows, n, p, (const char*)A_dev + r0 * n * es, B_dev, (char*)C_dev + r0 * p * es, dtype,
-                       stream)))
+  for (int64_t i = 1; i < P; ++i) {
+    if ((e = h2d_rows(A_host, A_dev, bnd[i], bnd[i + 1] - bnd[i], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
+    if ((e = cudaEventRecord(hp->evA[i], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  }
+  for (int64_t i = 0; i < P; ++i) {
+    const int64_t r0 = bnd[i], rows = bnd[i + 1] - bnd[i];
+    if ((e = cudaStreamWaitEvent(s, hp->evA[i], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    if (i == 0) {
+      for (int64_t j = 0; j < KB; ++j) {
+        if ((e = cudaStreamWaitEvent(s, hp->evB[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+        if (j > 0 && kb[j + 1] == kb[j]) continue;
+        if ((rc = moa_gemm_acc(rows, kb[j + 1] - kb[j], p, (const char*)A_dev + (r0 * n + kb[j]) * es,
+                               n > 0 ? n : 1, (const char*)B_dev + kb[j] * p * es, p > 0 ? p : 1,
+                               (char*)C_dev + r0 * p * es, p > 0 ? p : 1, j > 0 ? 1 : 0, dtype, stream)))
+          return rc;
+      }
+    } else if ((rc = moa_gemm(rows, n, p, (const char*)A_dev + r0 * n * es, B_dev, (char*)C_dev + r0 * p * es, dtype,
+                              stream))) {
       return rc;
-    if ((e = cudaEventRecord(hp->evC[j], s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-    if ((e = cudaStreamWaitEvent(hp->d2h, hp->evC[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    }
+    if ((e = cudaEventRecord(hp->evC[i], s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(hp->d2h, hp->evC[i], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     if (rows * p > 0 &&
         (e = cudaMemcpyAsync((char*)C_host + r0 * p * es, (const char*)C_dev + r0 * p * es, (size_t)(rows * p * es),
                              cudaMemcpyDeviceToHost, hp->d2h)) != cudaSuccess)
