@@ -37,6 +37,19 @@ sys.path.insert(0, ROOT)
 # held for a 125 ms sustained run). MEASURED_PEAKS.json carries no fp64 figure.
 FP64_DMMA_PEAK_TFLOPS = 37.0
 FP64_PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_probe.jsonl (MEASURED_PEAKS.json has no fp64 entry)"
+METRIC = "fp64 GEMM GFLOP/s (joules/GEMM vs N in energy/sweep)"
+DATA = "synthetic (seeded splitmix64 uniform[-1,1), inputs/)"
+
+
+def workload_config(N, ws):
+    """The config object both arms report (same workload, same keys)."""
+    rows = N
+    m_total = rows * ws
+    return {"workload": f"square fp64 GEMM m=n=p={N} per GPU (BASELINE configs[1], top of the 1024-8192 sweep)"
+                        + ("" if ws == 1 else f"; row-lifted over {ws} GPUs, m={m_total}, NCCL broadcast of B each step"),
+            "m": m_total, "n": N, "p": N, "rows_per_rank": rows,
+            "parallelism": "single GPU" if ws == 1 else f"row-lifted x{ws} (moa_gemm_lifted)",
+            "l2": f"inputs larger than L2 ({(rows * N + N * N + rows * N) * 8 / 2**20:.0f} MiB resident vs 126 MB L2), no flush"}
 
 
 def parse():
@@ -194,13 +207,15 @@ def run_reference(args):
         O.ip_rowblock(A, B)
     dt = time.perf_counter() - t0
     value = 2.0 * rows_per_step * n * p * args.steps / dt / 1e9
+    cfg = workload_config(N, max(1, args.gpus))
+    cfg["reference_sample"] = (f"each step runs the CPU oracle (literal ip.c, Fig. 3, unfused, single thread) on a "
+                               f"bounded sample of {rows_per_step} of the {m} rows; GFLOP/s = 2*rows*n*p / time")
     line = {
-        "impl": "reference", "metric": "fp64 GEMM GFLOP/s (CPU ONF oracle, literal ip.c)", "value": round(value, 4),
+        "impl": "reference", "metric": METRIC, "value": round(value, 4),
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 uniform[-1,1))",
-        "config": {"workload": f"square fp64 GEMM m=n=p={N} (BASELINE configs[1]); each step = a bounded row "
-                               f"sample of {rows_per_step} rows", "m": m, "n": n, "p": p},
+        "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": cfg,
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
                          "sample": f"{rows_per_step} rows x {args.steps} steps of the m=n=p={N} workload"},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -404,18 +419,15 @@ def main():
         dist.destroy_process_group()
     if rank != 0:
         return 0
+    cfg = workload_config(N, ws)
+    cfg["plan"] = {"kernel": plan.kernel, "bm": plan.bm, "bn": plan.bn, "bk": plan.bk, "stages": plan.stages,
+                   "grid": plan.grid, "tiles": plan.tiles}
     line = {
-        "metric": "fp64 GEMM GFLOP/s (joules/GEMM vs N in energy/sweep)", "value": round(value, 2),
+        "metric": METRIC, "value": round(value, 2),
         "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 uniform[-1,1), inputs/)",
-        "config": {"workload": f"square fp64 GEMM m=n=p={N} per GPU (BASELINE configs[1], top of the 1024-8192 sweep)"
-                               + ("" if ws == 1 else f"; row-lifted over {ws} GPUs, m={m_total}, NCCL broadcast of B each step"),
-                   "m": m_total, "n": n, "p": p, "rows_per_rank": rows,
-                   "parallelism": "single GPU" if ws == 1 else f"row-lifted x{ws} (moa_gemm_lifted)",
-                   "l2": f"inputs larger than L2 ({(rows * n + n * p + rows * p) * 8 / 2**20:.0f} MiB resident vs 126 MB L2), no flush",
-                   "plan": {"kernel": plan.kernel, "bm": plan.bm, "bn": plan.bn, "bk": plan.bk,
-                            "stages": plan.stages, "grid": plan.grid, "tiles": plan.tiles}},
+        "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": cfg,
         "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": round(achieved_tf / FP64_DMMA_PEAK_TFLOPS, 4),
                      "traffic": traffic, "kernel": "k_dgemm_tma (fp64 DMMA)", "kernel_ms": round(kern_ms, 4),
