@@ -198,7 +198,7 @@ def run_reference(args):
     O.ip_rowblock(A1, B)
     t_row = time.perf_counter() - t0
     total_budget = 150.0  # seconds for warmup + steps
-    rows_per_step = max(1, int(total_budget / max(t_row, 1e-6) / (args.steps + args.warmup)))
+    rows_per_step = max(1, min(m, int(total_budget / max(t_row, 1e-6) / (args.steps + args.warmup))))
     A = I.host_matrix(rows_per_step, n, 1, I.ID_A)
     for _ in range(args.warmup):
         O.ip_rowblock(A, B)
