@@ -320,8 +320,12 @@ def main():
             traffic = None
     plan = moa.plan(rows, n, p)
 
-    # energy (NVML, this rank's GPU; J per GEMM step)
+    # energy (NVML; J per GEMM step summed over every participating GPU)
     energy = None
+    if ws > 1:
+        t = torch.tensor([float((e1 - e0) if (e0 is not None and e1 is not None) else -1e30)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e0, e1 = (0.0, float(t.item())) if t.item() >= 0 else (None, None)
     if e0 is not None and e1 is not None:
         j = (e1 - e0) / 1e3
         energy = {"j_per_gemm": round(j / args.steps, 4), "window_s": round(elapsed_ms / 1e3, 3),
