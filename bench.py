@@ -329,7 +329,7 @@ def main():
     if e0 is not None and e1 is not None:
         j = (e1 - e0) / 1e3
         energy = {"j_per_gemm": round(j / args.steps, 4), "window_s": round(elapsed_ms / 1e3, 3),
-                  "avg_w": round(j / (elapsed_ms / 1e3), 1), "gflops_per_w": round(value / ws / (j / (elapsed_ms / 1e3)), 2)}
+                  "avg_w": round(j / (elapsed_ms / 1e3), 1), "gflops_per_w": round(value / (j / (elapsed_ms / 1e3)), 2)}
 
     # e2e through moa_gemm_host (host buffers, copies inside the timed region)
     e2e = None
