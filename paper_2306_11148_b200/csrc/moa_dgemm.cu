@@ -209,7 +209,7 @@ struct K1Traits {
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8;
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 3 * STAGES * 8;  // + tile id per stage
   static_assert(BM == 32 * WARPS_M, "warp tile is 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
                                   K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
-                int64_t tiles_m, int64_t tiles_n, int group) {
+                int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ tile_ctr) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -230,6 +230,12 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
+  // Tile id carried by each stage slot: the producer claims tiles (dynamically from
+  // tile_ctr, or statically by stride) and publishes the id with the slot's full
+  // barrier; -1 tells the consumers to stop. Dynamic claiming balances the work per
+  // SM whatever the CTA placement (the static stride left SMs 8 vs 6 tiles at 2
+  // CTAs/SM).
+  volatile int64_t* s_tile = reinterpret_cast<volatile int64_t*>(smem_raw + (empty0 + STAGES * 8 - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles = tiles_m * tiles_n;
   const int ktiles = (int)((n + kBK - 1) / kBK);
@@ -252,12 +258,14 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
       prefetch_tmap(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int64_t t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : (int64_t)blockIdx.x;
+      for (; t < tiles; t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : t + gridDim.x) {
         int64_t tm, tn;
         tile_coords(t, tiles_m, tiles_n, group, tm, tn);
         const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
         for (int kt = 0; kt < ktiles; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+          s_tile[stage] = t;
           const uint32_t fb = full0 + 8 * stage;
           mbar_arrive_expect_tx(fb, Tr::kStageBytes);
           const uint32_t sa = sbase + stage * Tr::kStageBytes;
@@ -270,6 +278,9 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
           }
         }
       }
+      mbar_wait(empty0 + 8 * stage, phase ^ 1u);  // end-of-work sentinel slot
+      s_tile[stage] = -1;
+      mbar_arrive(full0 + 8 * stage);
     }
     return;
   }
@@ -281,7 +292,10 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   Acc<Tr::kNBox> acc;
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  for (;;) {
+    mbar_wait(full0 + 8 * stage, phase);  // first slab of the next tile, or the sentinel
+    const int64_t t = s_tile[stage];
+    if (t < 0) break;
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     if constexpr (ACC)
@@ -289,7 +303,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     else
       acc_zero(acc);
     for (int kt = 0; kt < ktiles; ++kt) {
-      mbar_wait(full0 + 8 * stage, phase);
+      if (kt > 0) mbar_wait(full0 + 8 * stage, phase);
       const uint8_t* sa = sptr + stage * Tr::kStageBytes;
       mma_slab(acc, sa + wm * 32 * kRowBytes, sa + Tr::kABytes + wn * Tr::kNBox * kBoxBytes, f);
       __syncwarp();
@@ -378,8 +392,10 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
+  unsigned int* ctr = nullptr;
+  if (plan.tiles > plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                                       plan.raster_group);
+                                                       plan.raster_group, ctr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));

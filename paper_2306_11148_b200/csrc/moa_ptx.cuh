@@ -76,4 +76,9 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* 
                int box_cols, int box_rows, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B,
                int64_t ld = -1 /* row stride in elements; -1 = cols */);
 
+// Host: a zeroed device counter for one dynamically scheduled launch on `stream`
+// (a slot of a per-device pool allocated once; zeroed with cudaMemsetAsync on the
+// stream, so it is ordered before the kernel). Returns false (error set) on failure.
+bool acquire_tile_counter(cudaStream_t stream, unsigned int** out);
+
 }  // namespace moa

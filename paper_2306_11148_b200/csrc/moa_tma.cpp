@@ -1,6 +1,7 @@
 // moa_tma.cpp — host-side TMA descriptor encoding (cuTensorMapEncodeTiled via the
 // runtime's driver entry point, so libmoa.so needs no -lcuda).
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -41,6 +42,35 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* 
     set_error(buf);
     return false;
   }
+  return true;
+}
+
+namespace {
+constexpr int kCounterSlots = 4096;
+struct CounterPool {
+  unsigned int* dev = nullptr;
+  unsigned int next = 0;
+};
+std::mutex g_ctr_mu;
+std::map<int, CounterPool> g_ctr;
+}  // namespace
+
+bool acquire_tile_counter(cudaStream_t stream, unsigned int** out) {
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
+  unsigned int* slot = nullptr;
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_ctr_mu);
+    CounterPool& pool = g_ctr[device];
+    if (!pool.dev) e = cudaMalloc(&pool.dev, kCounterSlots * sizeof(unsigned int));  // library-owned, once
+    if (e == cudaSuccess) slot = pool.dev + (pool.next++ % kCounterSlots);
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(slot, 0, sizeof(unsigned int), stream);
+  if (e != cudaSuccess) {
+    set_error(std::string("tile counter: ") + cudaGetErrorString(e));
+    return false;
+  }
+  *out = slot;
   return true;
 }
 
