@@ -33,6 +33,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "moa_internal.h"
@@ -293,7 +294,11 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
-    mbar_wait(full0 + 8 * stage, phase);  // first slab of the next tile, or the sentinel
+    // Peek: wait for the first slab of the next tile (or the sentinel) and read its
+    // id. The k-loop below waits on the same, already complete, phase again — that
+    // keeps the loop body identical to the static version (a conditional wait inside
+    // it cost ~2.5%: reconvergence + non-uniform barrier addressing).
+    mbar_wait(full0 + 8 * stage, phase);
     const int64_t t = s_tile[stage];
     if (t < 0) break;
     int64_t tm, tn;
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     else
       acc_zero(acc);
     for (int kt = 0; kt < ktiles; ++kt) {
-      if (kt > 0) mbar_wait(full0 + 8 * stage, phase);
+      mbar_wait(full0 + 8 * stage, phase);
       const uint8_t* sa = sptr + stage * Tr::kStageBytes;
       mma_slab(acc, sa + wm * 32 * kRowBytes, sa + Tr::kABytes + wn * Tr::kNBox * kBoxBytes, f);
       __syncwarp();
@@ -393,7 +398,8 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     return MOA_ERR_CUDA;
   }
   unsigned int* ctr = nullptr;
-  if (plan.tiles > plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
+  static const bool force_static = getenv("MOA_STATIC_TILES") != nullptr;  // A/B knob (profiling only)
+  if (!force_static && plan.tiles > plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
                                                        plan.raster_group, ctr);
   cudaError_t e = cudaGetLastError();
