@@ -413,13 +413,13 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
 // The chooser's candidate lifted blocks. ctas_per_sm is refined at first use
 // from the occupancy API (registers are what limit it; see K1Traits). eta is the
 // per-tile efficiency relative to 128x128, measured once at N=16384 where wave
-// quantisation vanishes (profiles/r01_configs.json block_sweep: 0.9815 / 0.9722 /
-// 0.9599 of peak) — a property of the tile config, not a per-shape tuning.
+// quantisation vanishes (profiles/r01_configs.json block_sweep: 0.9838 / 0.9775 /
+// 0.9325 of peak) — a property of the tile config, not a per-shape tuning.
 TileConfig kK1Configs[] = {
     // kernel, bm, bn, bk, stages, threads, ctas/SM, smem, eta
     {MOA_KERNEL_DGEMM_TMA, 128, 128, 16, 6, K1Traits<128, 128, 4, 2, 6>::kThreads, 1, K1Traits<128, 128, 4, 2, 6>::kSmem, 1.00},
-    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 2, 4>::kThreads, 1, K1Traits<128, 64, 4, 2, 4>::kSmem, 0.99},
-    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 4, 4>::kThreads, 2, K1Traits<64, 64, 2, 4, 4>::kSmem, 0.978},
+    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 2, 4>::kThreads, 1, K1Traits<128, 64, 4, 2, 4>::kSmem, 0.994},
+    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 4, 4>::kThreads, 2, K1Traits<64, 64, 2, 4, 4>::kSmem, 0.948},
 };
 TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
