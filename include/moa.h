@@ -181,6 +181,18 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
 int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,
                          void* workspace, int dtype, void* stream, moa_comm_t comm);
 
+/* moa_gemm_lifted_2d — 2-D dimension lifting: the i axis over grid_rows and the j axis
+ * over grid_cols (grid_rows * grid_cols = G; rank = r * grid_cols + c). COLLECTIVE.
+ * Rank (r, c) owns rows [row0_r, row0_r + rows_r) = moa_lift_rows(m, grid_rows, r)
+ * and columns [col0_c, col0_c + cols_c) = moa_lift_rows(p, grid_cols, c):
+ *   A_panel : device, rows_r x n — input on (r, 0), broadcast along the process row;
+ *   B_panel : device, n x cols_c — input on (0, c), broadcast along the process column;
+ *   C_block : device, rows_r x cols_c, receives C[rows, cols].
+ * Row and column sub-communicators are split from `comm` (ncclCommSplit) on first
+ * use of a grid shape and cached in the communicator. Bitwise equal to one GPU. */
+int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
+                       void* C_block, int dtype, void* stream, moa_comm_t comm);
+
 /* moa_lift_panels — static k-panel count for the lifted exchange: 1 when B does
  * not travel (nranks == 1), else ceil(bytes(B) / 512 MiB) clamped to [1, 8] and
  * to n/64. Pure function. */

@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
-    "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols",
+    "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols", "gemm_lifted_2d",
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
@@ -64,6 +64,7 @@ _moa_gemm_lifted_ex = _sig("moa_gemm_lifted_ex", [_i64, _i64, _i64, _vp, _vp, _v
 _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp])
 _moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
 _moa_gemm_lifted_cols = _sig("moa_gemm_lifted_cols", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
+_moa_gemm_lifted_2d = _sig("moa_gemm_lifted_2d", [_i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_hadamard = _sig("moa_hadamard", [_i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_kron = _sig("moa_kron", [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_psi = _sig("moa_psi", [_i32, ctypes.POINTER(_i64), _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
@@ -379,3 +380,17 @@ def gemm_lifted_cols(A, B_local, C_local, p: int, comm: Comm, C_full=None, works
                                  None if workspace is None else (workspace.data_ptr() or None), code,
                                  _stream_ptr(stream), comm.handle), "moa_gemm_lifted_cols")
     return C_local
+
+
+def gemm_lifted_2d(m: int, p: int, grid_rows: int, grid_cols: int, A_panel, B_panel, C_block, comm: Comm, *,
+                   stream=None):
+    """2-D lifted C := A • B on a grid_rows x grid_cols process grid (moa_gemm_lifted_2d)."""
+    n = A_panel.shape[1]
+    code = _dtype_code(A_panel)
+    for name, t in (("A_panel", A_panel), ("B_panel", B_panel), ("C_block", C_block)):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    _check(_moa_gemm_lifted_2d(m, n, p, grid_rows, grid_cols, A_panel.data_ptr() or None, B_panel.data_ptr() or None,
+                               C_block.data_ptr() or None, code, _stream_ptr(stream), comm.handle),
+           "moa_gemm_lifted_2d")
+    return C_block

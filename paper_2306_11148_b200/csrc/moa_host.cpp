@@ -28,6 +28,9 @@ struct moa_comm_s {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr;
   cudaEvent_t ev_panel[kMaxPanels] = {};
+  // 2-D lifting: row / column sub-communicators for the last grid shape used
+  int grid_rows = 0, grid_cols = 0;
+  ncclComm_t row_comm = nullptr, col_comm = nullptr;
 };
 
 namespace moa {
@@ -619,6 +622,8 @@ int moa_comm_init(int nranks, int rank, const unsigned char id[128], int device,
 
 int moa_comm_destroy(moa_comm_t comm) {
   if (!comm) return MOA_OK;
+  if (comm->row_comm) ncclCommDestroy(comm->row_comm);
+  if (comm->col_comm) ncclCommDestroy(comm->col_comm);
   if (comm->side) cudaStreamSynchronize(comm->side);
   for (int i = 0; i < kMaxPanels; ++i)
     if (comm->ev_panel[i]) cudaEventDestroy(comm->ev_panel[i]);
@@ -861,6 +866,47 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
     }
   }
   return MOA_OK;
+}
+
+int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
+                       void* C_block, int dtype, void* stream, moa_comm_t comm) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (grid_rows <= 0 || grid_cols <= 0 || grid_rows * grid_cols != comm->nranks || m < 0 || p < 0) {
+    set_error("grid_rows * grid_cols must equal the number of ranks");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  const int r = comm->rank / grid_cols, c = comm->rank % grid_cols;
+  int64_t row0, rows, col0, cols;
+  int rc = moa_lift_rows(m, grid_rows, r, &row0, &rows);
+  if (!rc) rc = moa_lift_rows(p, grid_cols, c, &col0, &cols);
+  if (rc) return rc;
+  if ((rc = validate(rows, n, cols, A_panel, B_panel, C_block, dtype))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const ncclDataType_t ty = nccl_type(dtype);
+  if (comm->nranks > 1) {
+    if (comm->grid_rows != grid_rows || comm->grid_cols != grid_cols) {  // (re)split, collective
+      if (comm->row_comm) ncclCommDestroy(comm->row_comm);
+      if (comm->col_comm) ncclCommDestroy(comm->col_comm);
+      comm->row_comm = comm->col_comm = nullptr;
+      ncclResult_t q = ncclCommSplit(comm->nccl, r, c, &comm->row_comm, nullptr);
+      if (q == ncclSuccess) q = ncclCommSplit(comm->nccl, c, r, &comm->col_comm, nullptr);
+      if (q != ncclSuccess) return nccl_fail(q, "ncclCommSplit");
+      comm->grid_rows = grid_rows;
+      comm->grid_cols = grid_cols;
+    }
+    // A's row panel travels along the process row (root: column 0), B's column panel
+    // along the process column (root: row 0): the i axis lifted over grid rows, the
+    // j axis over grid columns (Figs. 4 and 5 together).
+    ncclResult_t q = ncclSuccess;
+    if (grid_cols > 1 && rows * n > 0) q = ncclBroadcast(A_panel, A_panel, (size_t)(rows * n), ty, 0, comm->row_comm, s);
+    if (q == ncclSuccess && grid_rows > 1 && n * cols > 0)
+      q = ncclBroadcast(B_panel, B_panel, (size_t)(n * cols), ty, 0, comm->col_comm, s);
+    if (q != ncclSuccess) return nccl_fail(q, "ncclBroadcast(2-D panels)");
+  }
+  return moa_gemm(rows, n, cols, A_panel, B_panel, C_block, dtype, stream);
 }
 
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,

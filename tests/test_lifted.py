@@ -201,3 +201,77 @@ def test_lifted_cols_nccl_single_rank(cuda_device):
     finally:
         comm.close()
         dist.destroy_process_group()
+
+
+
+def _worker_2d(rank, world, port, gr, gc, m, n, p, q):
+    """2-D lifting on a gr x gc process grid (gloo): A row panels travel along process
+    rows, B column panels along process columns; the assembled C equals the oracle."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_11148_b200 as moa
+        from inputs import inputs as I
+        from oracle import oracle as O
+        r, c = rank // gc, rank % gc
+        r0, rows = moa.lift_rows(m, gr, r)
+        c0, cols = moa.lift_rows(p, gc, c)
+        groups_r = [dist.new_group([i * gc + j for j in range(gc)]) for i in range(gr)]
+        groups_c = [dist.new_group([i * gc + j for i in range(gr)]) for j in range(gc)]
+        A_panel = torch.from_numpy(I.host_matrix(rows, n, 5, I.ID_A, row0=r0)) if c == 0 else torch.zeros((rows, n), dtype=torch.float64)
+        Bfull = I.host_matrix(n, p, 5, I.ID_B)
+        B_panel = torch.from_numpy(np.ascontiguousarray(Bfull[:, c0:c0 + cols])) if r == 0 else torch.zeros((n, cols), dtype=torch.float64)
+        dist.broadcast(A_panel, src=r * gc, group=groups_r[r])
+        dist.broadcast(B_panel, src=c, group=groups_c[c])
+        C_block = torch.from_numpy(O.ip(A_panel.numpy(), B_panel.numpy(), fused=True))
+        gathered = [None] * world if rank == 0 else None
+        dist.gather_object((r0, rows, c0, cols, C_block.numpy()), gathered, dst=0)
+        if rank == 0:
+            C = np.full((m, p), np.nan)
+            for (a, ra, b, cb, blk) in gathered:
+                C[a:a + ra, b:b + cb] = blk
+            A = I.host_matrix(m, n, 5, I.ID_A)
+            q.put(bool(np.array_equal(C, O.ip(A, Bfull, fused=True))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_2d_lifting_host_logic_gloo_2x2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d, args=(r, 4, port, 2, 2, 21, 12, 19, q)) for r in range(4)]
+    for pr in procs:
+        pr.start()
+    ok = q.get(timeout=180)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert ok
+
+
+@pytest.mark.gpu
+def test_lifted_2d_nccl_single_rank(cuda_device):
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        m, n, p = 200, 96, 136
+        A = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+        B = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+        I.device_fill(A, 8, I.ID_A)
+        I.device_fill(B, 8, I.ID_B)
+        C = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+        moa.gemm_lifted_2d(m, p, 1, 1, A, B, C, comm)
+        torch.cuda.synchronize()
+        assert torch.equal(C, moa.gemm(A, B))
+        with pytest.raises(moa.MoAError):
+            moa.gemm_lifted_2d(m, p, 2, 1, A, B, C, comm)  # grid does not match the rank count
+    finally:
+        comm.close()
+        dist.destroy_process_group()
