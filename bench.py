@@ -118,7 +118,8 @@ class ClockSampler:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((sm, pw, rs))
+                tc = nv.nvmlDeviceGetTemperature(self.h, nv.NVML_TEMPERATURE_GPU)
+                self.samples.append((sm, pw, rs, tc))
             except Exception:
                 pass
             time.sleep(self.period)
@@ -145,7 +146,18 @@ class ClockSampler:
         reasons = [name for bit, name in self.REASONS.items() if mask & bit and bit != 0x1]
         return {"sm_mhz": statistics.median(s[0] for s in loaded), "sm_max_mhz": self.max_mhz,
                 "reasons": reasons, "power_w_median": round(statistics.median(s[1] for s in loaded), 1),
+                "temp_c_median": statistics.median(s[3] for s in loaded), "temp_c_max": max(s[3] for s in loaded),
                 "samples": len(loaded)}
+
+    def idle_watts(self, seconds: float = 1.0):
+        """Idle-power baseline: NVML energy over a quiet window (J/s)."""
+        e0 = self.energy_mj()
+        if e0 is None:
+            return None
+        t0 = time.perf_counter()
+        time.sleep(seconds)
+        e1 = self.energy_mj()
+        return round((e1 - e0) / 1e3 / (time.perf_counter() - t0), 1)
 
 
 def dist_env():
@@ -271,6 +283,8 @@ def main():
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    idle_w = sampler.idle_watts(1.0)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if ws > 1:
@@ -328,7 +342,10 @@ def main():
         e0, e1 = (0.0, float(t.item())) if t.item() >= 0 else (None, None)
     if e0 is not None and e1 is not None:
         j = (e1 - e0) / 1e3
-        energy = {"j_per_gemm": round(j / args.steps, 4), "window_s": round(elapsed_ms / 1e3, 3),
+        idle_j = (idle_w or 0.0) * ws * (elapsed_ms / 1e3)
+        energy = {"j_per_gemm": round(j / args.steps, 4), "idle_w": idle_w,
+                  "j_per_gemm_above_idle": round((j - idle_j) / args.steps, 4) if idle_w is not None else None,
+                  "window_s": round(elapsed_ms / 1e3, 3),
                   "avg_w": round(j / (elapsed_ms / 1e3), 1), "gflops_per_w": round(value / (j / (elapsed_ms / 1e3)), 2)}
 
     # e2e through moa_gemm_host (host buffers, copies inside the timed region)

@@ -49,7 +49,14 @@ def timed(fn, window_s, sampler, est_s):
     if e0 is not None and e1 is not None:
         out["j_per_gemm"] = round((e1 - e0) / 1e3 / reps, 6)
         out["avg_w"] = round((e1 - e0) / 1e3 / (ms * reps / 1e3), 1)
+        if IDLE_W[0] is not None:
+            out["j_per_gemm_above_idle"] = round(((e1 - e0) / 1e3 - IDLE_W[0] * ms * reps / 1e3) / reps, 6)
+    summ = sampler.summary()
+    out["temp_c_max"] = summ.get("temp_c_max")
     return out
+
+
+IDLE_W = [None]
 
 
 def mats(m, n, p, dtype):
@@ -117,8 +124,11 @@ def main():
     a = ap.parse_args()
     secs = set(a.sections.split(","))
     sampler = ClockSampler(0, period=0.1)
-    out = {"device": torch.cuda.get_device_name(0), "fp64_peak_tflops": FP64_DMMA_PEAK_TFLOPS,
-           "ffma_peak_tflops": FFMA_PEAK_TFLOPS, "time": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    torch.cuda.synchronize()
+    IDLE_W[0] = sampler.idle_watts(2.0)  # 2 s idle window
+    out = {"idle_w": IDLE_W[0]}
+    out.update({"device": torch.cuda.get_device_name(0), "fp64_peak_tflops": FP64_DMMA_PEAK_TFLOPS,
+           "ffma_peak_tflops": FFMA_PEAK_TFLOPS, "time": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())})
 
     if "ipophp" in secs:
         out["ipophp"] = ipophp(a, sampler)
