@@ -129,7 +129,8 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
  * row lifting: B goes first, then A in row panels on a library-owned
  * copy stream; each panel's GEMM runs on `stream` as soon as its rows arrive and
  * its C rows stream back on a second copy stream, so H2D, compute and D2H overlap.
- * Bitwise identical to copy + moa_gemm + copy. Host buffers should be pinned.
+ * Bitwise identical to copy + moa_gemm + copy (for MOA_F32_3XTF32, B is not split
+ * into k-panels, so this holds for every dtype). Host buffers should be pinned.
  * Same validation as moa_gemm on the device buffers; host pointers must be
  * non-NULL when their extents are non-zero. */
 int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
@@ -161,7 +162,8 @@ int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* 
  * byte range in MoA row-major order), broadcast one after the other on a
  * library-owned side stream, and the rank's compute for panel j (moa_gemm_acc,
  * accumulate for j > 0) waits only for panel j — the exchange overlaps the
- * lifted compute. Results are bitwise identical to npanels = 1. 1 <= npanels <= 16. */
+ * lifted compute. Results are bitwise identical to npanels = 1 for MOA_F64 and
+ * MOA_F32 (for MOA_F32_3XTF32 they agree within its tolerance). 1 <= npanels <= 16. */
 int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                        int dtype, void* stream, moa_comm_t comm, int npanels);
 

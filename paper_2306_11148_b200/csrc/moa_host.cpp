@@ -519,7 +519,7 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   // B itself is consumed in KB contiguous k-row panels by the FIRST row panel (an
   // accumulate chain, bitwise the one-call result), so its transfer overlaps compute
   // too; later row panels run after all of B has landed.
-  int64_t KB = (P > 1 && n >= 256) ? 4 : 1;
+  int64_t KB = (P > 1 && n >= 256 && dtype != MOA_F32_3XTF32) ? 4 : 1;  // chains are bitwise for f64/f32 only
   int64_t kb[kMaxHostPanels + 1];
   for (int64_t j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
   if ((e = cudaEventRecord(hp->ev0, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
