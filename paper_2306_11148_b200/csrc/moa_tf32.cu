@@ -45,6 +45,13 @@ constexpr int kBBox = 32 * kRowBytes;        // one B box: 32 k-rows x 32 floats
 constexpr int kThreads = 10 * 32;
 constexpr int kConvThreads = 128;
 
+// Instruction descriptor: D fp32 (c_format=1 @4), A,B tf32 (=2 @7, @10), A K-major
+// (bit15=0), B MN-major (bit16=1), N>>3 @17, M>>4 @24.
+constexpr uint32_t tf32_idesc(int bn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(bn >> 3) << 17) |
+         ((uint32_t)(kBM >> 4) << 24);
+}
+
 template <int BN, int STAGES>
 struct K4Traits {
   static constexpr int kBBytes = (BN / 32) * kBBox;
@@ -54,10 +61,7 @@ struct K4Traits {
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = 1024 + STAGES * kStageBytes + (3 * STAGES + 4) * 8 + 16;
   static_assert(kTmemCols <= 512, "TMEM has 512 columns");
-  // Instruction descriptor: D fp32 (c_format=1 @4), A,B tf32 (=2 @7, @10), A K-major
-  // (bit15=0), B MN-major (bit16=1), N>>3 @17, M>>4 @24.
-  static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                                     ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+  static constexpr uint32_t kIdesc = tf32_idesc(BN);
 };
 
 // ---------------------------- tcgen05 helpers ----------------------------------
@@ -324,7 +328,7 @@ struct K4TSTraits {
   static constexpr int kTmemCols = 512;
   static constexpr int kSmem = 1024 + STAGES * kStageBytes + (3 * STAGES + 4) * 8 + 16;
   static_assert(kAccBufs * BN + 64 * STAGES <= 512, "TMEM columns");
-  static constexpr uint32_t kIdesc = K4Traits<BN, STAGES>::kIdesc;
+  static constexpr uint32_t kIdesc = tf32_idesc(BN);
 };
 
 template <int BN, int STAGES>
