@@ -507,19 +507,35 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   // the panel GEMMs lose no wave efficiency; results are bitwise the one-call ones.
   moa_plan_t pl;
   if ((rc = moa_plan(m, n, p, dtype, ds.device, &pl))) return rc;
-  int64_t P = 1;
-  if (pl.kernel != MOA_KERNEL_NONE && pl.tiles > 0 && pl.bm > 0) {
-    P = pl.tiles / ((int64_t)ds.sms * 7);
-    if (P < 1) P = 1;
-    if (P > kMaxHostPanels) P = kMaxHostPanels;
-    if (P > pl.tiles_m) P = pl.tiles_m;
-  }
+  // Static schedule from the hardware shape (no measurement):
+  //  * row panel 0 consumes B in KB contiguous k-row panels as they land (an
+  //    accumulate chain, bitwise the one-call result for f64/f32), so it is sized
+  //    to compute about as long as B takes to cross the host link:
+  //    rows0 ~ peak_flops * esize / (2 * link_bytes_per_s), independent of n and p
+  //    (fp64: 37 TF/s * 8 B / (2 * ~52 GB/s) ~ 2.8K rows -> 3072; fp32: 2304);
+  //  * the remaining rows go in panels of ~7 waves of tiles (no wave loss), each
+  //    starting when its A rows have landed, after all of B.
+  const bool chain = n >= 512 && dtype != MOA_F32_3XTF32;
+  const int64_t bm = pl.bm > 0 ? pl.bm : 128;
   int64_t bnd[kMaxHostPanels + 1];
-  for (int64_t j = 0; j <= P; ++j) bnd[j] = j == P ? m : (pl.tiles_m * j / P) * (pl.bm > 0 ? pl.bm : 1);
-  // B itself is consumed in KB contiguous k-row panels by the FIRST row panel (an
-  // accumulate chain, bitwise the one-call result), so its transfer overlaps compute
-  // too; later row panels run after all of B has landed.
-  int64_t KB = (P > 1 && n >= 256 && dtype != MOA_F32_3XTF32) ? 4 : 1;  // chains are bitwise for f64/f32 only
+  int64_t P = 0;
+  bnd[0] = 0;
+  if (pl.kernel != MOA_KERNEL_NONE && pl.tiles > 0) {
+    const int64_t rows0 = chain ? (dtype == MOA_F64 ? 3072 : 2304) : 0;
+    const int64_t per = (ds.sms * 7 / (pl.tiles_n > 0 ? pl.tiles_n : 1) + 1) * bm;  // ~7 waves of tiles
+    int64_t r = rows0 > 0 && rows0 < m ? rows0 : 0;
+    if (r > 0) bnd[++P] = r;
+    const int64_t rest = m - r;
+    int64_t k = (rest + per - 1) / per;
+    if (k < 1) k = 1;
+    if (k > kMaxHostPanels - P) k = kMaxHostPanels - P;
+    for (int64_t j = 1; j <= k; ++j) bnd[P + j] = j == k ? m : r + (((rest / bm) * j / k) * bm);
+    P += k;
+  } else {
+    bnd[++P] = m;
+  }
+  const bool first_chain = chain && P > 1;
+  const int64_t KB = first_chain ? 8 : 1;
   int64_t kb[kMaxHostPanels + 1];
   for (int64_t j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
   if ((e = cudaEventRecord(hp->ev0, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
