@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     // keeps the loop body identical to the static version (a conditional wait inside
     // it cost ~2.5%: reconvergence + non-uniform barrier addressing).
     mbar_wait(full0 + 8 * stage, phase);
-    const int64_t t = s_tile[stage];
+    __syncwarp();  // reconverge the lanes of the spin before reading the id / mma.sync
+    const int64_t t = __shfl_sync(0xffffffffu, s_tile[stage], 0);  // one id per warp
     if (t < 0) break;
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
