@@ -508,16 +508,16 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   moa_plan_t pl;
   if ((rc = moa_plan(m, n, p, dtype, ds.device, &pl))) return rc;
   // Static schedule from the hardware shape (no measurement):
-  //  * row panel 0 is computed as a chain over KB k-panels (accumulate, bitwise the
-  //    one-call result for f64/f32); for each k-panel j the H2D stream ships A0's
-  //    column slice A0[:, Kj] (one strided 2-D copy) and B's rows Kj (one contiguous
-  //    range, MoA order), so compute starts after the first pair. rows0 is the
-  //    smallest panel whose per-pair compute covers the pair's transfer:
-  //      2*rows0*w*p/peak >= (rows0 + p)*w*es/link
-  //      => rows0 >= (p*es/link) / (2p/peak - es/link)
-  //    with the part's DMMA/FFMA2 peak and a ~52 GB/s host link (PCIe 5 x16).
-  //  * the remaining rows go in panels of ~7 waves of tiles (no wave loss), each
-  //    starting when its A rows have landed, after all of B.
+  //  * row panel 0 is computed as a chain over KB = 8 k-panels of B (accumulate,
+  //    bitwise the one-call result for f64/f32) that start as soon as A0 and the
+  //    first B k-panel have landed; it is sized so its compute lasts about as long
+  //    as B takes to cross the host link: rows0 ~ peak * esize / (2 * link), independent
+  //    of n and p (fp64: 37 TF/s * 8 B / (2 * 52 GB/s) ~ 2.9K rows);
+  //  * the middle rows go in panels of ~7 waves of tiles (no wave loss), each
+  //    starting when its A rows have landed, after all of B;
+  //  * a short last panel (4 tile rows) trims the final D2H tail.
+  // (Shipping A0 as strided column slices with each B k-panel was tried and lost:
+  //  strided 2-D host copies do not reach the contiguous PCIe rate.)
   const bool chain = n >= 512 && dtype != MOA_F32_3XTF32;
   const int64_t bm = pl.bm > 0 ? pl.bm : 128;
   int64_t bnd[kMaxHostPanels + 1];
@@ -527,19 +527,19 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
     int64_t rows0 = 0;
     if (chain) {
       const double peak = dtype == MOA_F64 ? 37.0e12 : 61.0e12, link = 52.0e9;
-      const double den = 2.0 * (double)p / peak - (double)es / link;
-      rows0 = den > 0 ? (int64_t)((double)p * es / link / den) : m;
-      rows0 = (rows0 + bm - 1) / bm * bm;
+      rows0 = ((int64_t)(peak * es / (2.0 * link)) + bm - 1) / bm * bm;
       if (rows0 > m / 2) rows0 = 0;  // too small a problem to pipeline this way
     }
     const int64_t per = (ds.sms * 7 / (pl.tiles_n > 0 ? pl.tiles_n : 1) + 1) * bm;  // ~7 waves of tiles
+    const int64_t last = (m - rows0 > 2 * per) ? 4 * bm : 0;
     if (rows0 > 0) bnd[++P] = rows0;
-    const int64_t rest = m - rows0;
+    const int64_t rest = m - rows0 - last;
     int64_t k = (rest + per - 1) / per;
     if (k < 1) k = 1;
-    if (k > kMaxHostPanels - P) k = kMaxHostPanels - P;
-    for (int64_t j = 1; j <= k; ++j) bnd[P + j] = j == k ? m : rows0 + (((rest / bm) * j / k) * bm);
+    if (k > kMaxHostPanels - P - 1) k = kMaxHostPanels - P - 1;
+    for (int64_t j = 1; j <= k; ++j) bnd[P + j] = j == k ? rows0 + rest : rows0 + (((rest / bm) * j / k) * bm);
     P += k;
+    if (last > 0) bnd[++P] = m;
   } else {
     bnd[++P] = m;
   }
@@ -555,20 +555,11 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
     return cudaMemcpyAsync((char*)ddst + r0 * rowlen * es, (const char*)hsrc + r0 * rowlen * es,
                            (size_t)(rows * rowlen * es), cudaMemcpyHostToDevice, hp->h2d);
   };
-  // copy order on the H2D engine: (A0[:, Kj], B[Kj]) pairs (or all of A0 then B when
-  // not chaining), then A panels 1..P-1
-  if (!first_chain) {
-    if ((e = h2d_rows(A_host, A_dev, bnd[0], bnd[1] - bnd[0], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
-  }
+  // copy order on the H2D engine: A panel 0, B's k-panels, A panels 1..P-1
+  if ((e = h2d_rows(A_host, A_dev, bnd[0], bnd[1] - bnd[0], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
   if ((e = cudaEventRecord(hp->evA[0], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   for (int64_t j = 0; j < KB; ++j) {
-    const int64_t w = kb[j + 1] - kb[j];
-    if (first_chain && w > 0 && bnd[1] > 0 &&
-        (e = cudaMemcpy2DAsync((char*)A_dev + kb[j] * es, (size_t)(n * es), (const char*)A_host + kb[j] * es,
-                               (size_t)(n * es), (size_t)(w * es), (size_t)bnd[1], cudaMemcpyHostToDevice,
-                               hp->h2d)) != cudaSuccess)
-      return cuda_fail(e, "H2D A0 column slice");
-    if ((e = h2d_rows(B_host, B_dev, kb[j], w, p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
+    if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
     if ((e = cudaEventRecord(hp->evB[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   }
   for (int64_t i = 1; i < P; ++i) {
