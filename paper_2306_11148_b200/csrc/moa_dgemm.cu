@@ -153,8 +153,8 @@ __device__ __forceinline__ void load_acc(Acc<NBOX>& c, const double* __restrict_
         // would pair registers of different DMMA operands and cost copies)
         double lo = 0.0, hi = 0.0;
         if (r < m) {
-          if (col < p) lo = crow[col];
-          if (col + 1 < p) hi = crow[col + 1];
+          if (col < p) lo = __ldcg(crow + col);  // L2: may be another CTA's partial
+          if (col + 1 < p) hi = __ldcg(crow + col + 1);
         }
         c.v[a][b][0][q] = lo;
         c.v[a][b][1][q] = hi;
@@ -200,7 +200,7 @@ struct K1Traits {
   static constexpr int kNBoxW = BN / WARPS_N / 16;
   // Only the 32x64 warp tile (64 accumulators) needs the producer's registers.
   static constexpr int kProducerWarps = (kConsumerWarps >= 8 && kNBoxW == 4) ? 4 : 1;
-  static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : 2;  // 32x16 warp tiles fit 2 CTAs/SM (96 regs)
+  static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : 2;  // 32x16 warp tiles fit 2 CTAs/SM
   static constexpr bool kSetMaxNReg = kProducerWarps == 4;
   static constexpr int kProducerRegs = 40;
   static constexpr int kConsumerRegs = 232;
@@ -210,20 +210,68 @@ struct K1Traits {
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 3 * STAGES * 8;  // + tile id per stage
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 16 * STAGES + 64;  // + descriptors, sk plan
   static_assert(BM == 32 * WARPS_M, "warp tile is 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
 
-// ACC (compile time, so the plain path keeps ptxas's in-place accumulator
-// allocation: a runtime flag made it insert register copies around every DMMA,
-// -5.4% at N=16384): start each tile's chain from the C in memory.
+// One piece of work for a consumer warp: tile (row0, col0), k-slabs [k0, k1). With
+// `load` the chain starts from the C in memory (accumulate mode, or the stored
+// low-k partial of a split tile), else from +0: the loads are predicated off by
+// passing m = 0, so there is ONE copy of the slab loop in the kernel (a branch
+// between load_acc and acc_zero once cost 5.4% in register copies).
+template <int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
+__device__ __forceinline__ void consume_piece(Acc<NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
+                                              int& stage, uint32_t& phase, double* __restrict__ C, int64_t m,
+                                              int64_t p, int64_t ldc, int64_t row0, int64_t col0, int wm, int wn,
+                                              int k0, int k1, bool load, const FragOffsets& f, int lane) {
+  load_acc<NBOX, true>(acc, C, load ? m : 0, p, ldc, row0 + wm * 32, col0 + wn * NBOX * 16, f);
+  for (int kt = k0; kt < k1; ++kt) {
+    mbar_wait(full0 + 8 * stage, phase);  // (ptxas reconverges the spin with BSSY/BSYNC before the DMMAs)
+    const uint8_t* sa = sptr + stage * STAGE_BYTES;
+    mma_slab(acc, sa + wm * 32 * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
+    // WAR across proxies: these generic-proxy LDS reads must be ordered before the
+    // producer's next TMA (async-proxy) write of this stage. The arrive's .release
+    // alone does not do it (ptxas even hoists the arrive above the slab's last
+    // DMMAs): without this fence whole warp tiles were computed from overwritten
+    // operands, rarely under dynamic scheduling, often under stream-K.
+#ifndef MOA_AB_NO_PROXY_FENCE  // A/B cost measurement only (tools/build_variant.sh); never set in the product
+    fence_proxy_async_smem();
+#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+  store_acc<NBOX, true>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * NBOX * 16, f);
+}
+
+// ACC: start every tile's chain from the C in memory (moa_gemm_acc k-panel chains).
+//
+// Work assignment (the producer decides; the consumers only read piece descriptors):
+//  * flags != null — stream-K (moa_ptx.cuh sk_plan): static, balanced runs of
+//    k-slabs; pieces head, data-parallel tiles, whole stream-K tiles, tail. Used
+//    for few waves, where the last partial wave costs most.
+//  * tile_ctr != null — dynamic: whole tiles claimed from an atomic counter. Used
+//    for many waves: claiming keeps all CTAs of a wave in k-lockstep, so they share
+//    the A/B k-slabs in L2 (a static schedule drifts: 53% L2 hits vs 82%, N=16384).
+//  * neither — static stride (tiles <= grid).
+// The producer publishes each piece (tile, k0, k1) in the slot of its first stage,
+// before that stage's full-barrier arrive (release); t = -1 ends the work.
+struct PieceDesc {
+  int64_t t;
+  int32_t k0, k1;
+};
+
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC>
 __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads,
                                   K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
-                int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ tile_ctr) {
+                int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ flags,
+                unsigned int* __restrict__ tile_ctr) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -231,14 +279,9 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
-  // Tile id carried by each stage slot: the producer claims tiles (dynamically from
-  // tile_ctr, or statically by stride) and publishes the id with the slot's full
-  // barrier; -1 tells the consumers to stop. Dynamic claiming balances the work per
-  // SM whatever the CTA placement (the static stride left SMs 8 vs 6 tiles at 2
-  // CTAs/SM).
-  volatile int64_t* s_tile = reinterpret_cast<volatile int64_t*>(smem_raw + (empty0 + STAGES * 8 - raw));
+  volatile PieceDesc* desc = reinterpret_cast<volatile PieceDesc*>(smem_raw + (empty0 + STAGES * 8 - raw));
+  SkPieces* skq = reinterpret_cast<SkPieces*>(smem_raw + (empty0 + STAGES * 8 + 16 * STAGES - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tiles = tiles_m * tiles_n;
   const int ktiles = (int)((n + kBK - 1) / kBK);
 
   if (threadIdx.x == 0) {
@@ -248,6 +291,8 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
       mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
     }
     fence_mbar_init();
+    // the stream-K plan is computed here, not by the producer (40 registers there)
+    if (flags) *skq = sk_pieces(tiles_m * tiles_n, ktiles, gridDim.x, blockIdx.x);
   }
   __syncthreads();
 
@@ -259,28 +304,44 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
       prefetch_tmap(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      int64_t t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : (int64_t)blockIdx.x;
-      for (; t < tiles; t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : t + gridDim.x) {
+      auto emit = [&](int64_t t, int k0, int k1) {
         int64_t tm, tn;
         tile_coords(t, tiles_m, tiles_n, group, tm, tn);
         const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
-        for (int kt = 0; kt < ktiles; ++kt) {
+        for (int kt = k0; kt < k1; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1u);
-          s_tile[stage] = t;
+          if (kt == k0) {
+            desc[stage].t = t;
+            desc[stage].k0 = k0;
+            desc[stage].k1 = k1;
+          }
           const uint32_t fb = full0 + 8 * stage;
           mbar_arrive_expect_tx(fb, Tr::kStageBytes);
           const uint32_t sa = sbase + stage * Tr::kStageBytes;
           tma_load_2d(sa, &tmA, fb, kt * kBK, row0);
 #pragma unroll
-          for (int b = 0; b < BN / 16; ++b) tma_load_2d(sa + Tr::kABytes + b * kBoxBytes, &tmB, fb, col0 + 16 * b, kt * kBK);
+          for (int b = 0; b < BN / 16; ++b)
+            tma_load_2d(sa + Tr::kABytes + b * kBoxBytes, &tmB, fb, col0 + 16 * b, kt * kBK);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
           }
         }
+      };
+      const int64_t tiles = tiles_m * tiles_n;
+      if (flags) {
+        const int64_t np = skq->npieces;
+        for (int64_t i = 0; i < np; ++i) {
+          const Piece pc = piece_at(skq, i, ktiles, gridDim.x, blockIdx.x);
+          emit(pc.t, pc.k0, pc.k1);
+        }
+      } else {
+        for (int64_t t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : (int64_t)blockIdx.x; t < tiles;
+             t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : t + gridDim.x)
+          emit(t, 0, ktiles);
       }
       mbar_wait(empty0 + 8 * stage, phase ^ 1u);  // end-of-work sentinel slot
-      s_tile[stage] = -1;
+      desc[stage].t = -1;
       mbar_arrive(full0 + 8 * stage);
     }
     return;
@@ -289,37 +350,32 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   // ------------------------------- consumers ---------------------------------
   if constexpr (Tr::kSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Tr::kConsumerRegs));
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-  const FragOffsets f = make_offsets(lane);
+  FragOffsets f = make_offsets(lane);
+  // Opaque copies: computed once, kept live. Without this ptxas rematerialised the
+  // offsets (S2R tid + ~25 integer ops) in every slab.
+#pragma unroll
+  for (int s = 0; s < 4; ++s) asm volatile("" : "+r"(f.a[s]));
+  asm volatile("" : "+r"(f.b[0]), "+r"(f.b[1]));
   Acc<Tr::kNBox> acc;
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
-    // Peek: wait for the first slab of the next tile (or the sentinel) and read its
-    // id. The k-loop below waits on the same, already complete, phase again — that
-    // keeps the loop body identical to the static version (a conditional wait inside
-    // it cost ~2.5%: reconvergence + non-uniform barrier addressing).
+    // Peek: wait for the first stage of the next piece and read its descriptor
+    // (consume_piece waits on the same, already complete, phase again).
     mbar_wait(full0 + 8 * stage, phase);
-    __syncwarp();  // reconverge the lanes of the spin before reading the id / mma.sync
-    const int64_t t = __shfl_sync(0xffffffffu, s_tile[stage], 0);  // one id per warp
+    __syncwarp();
+    const int64_t t = desc[stage].t;
     if (t < 0) break;
+    const int k0 = desc[stage].k0, k1 = desc[stage].k1;
+    const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
+    if (tail) split_wait(flags + blockIdx.x, Tr::kConsumerWarps, lane);
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
-    if constexpr (ACC)
-      load_acc<Tr::kNBox, true>(acc, C, m, p, ldc, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
-    else
-      acc_zero(acc);
-    for (int kt = 0; kt < ktiles; ++kt) {
-      mbar_wait(full0 + 8 * stage, phase);
-      const uint8_t* sa = sptr + stage * Tr::kStageBytes;
-      mma_slab(acc, sa + wm * 32 * kRowBytes, sa + Tr::kABytes + wn * Tr::kNBox * kBoxBytes, f);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
-      }
-    }
-    store_acc<Tr::kNBox, true>(acc, C, m, p, ldc, tm * BM + wm * 32, tn * BN + wn * Tr::kNBox * 16, f);
+    consume_piece<Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(acc, sptr, full0, empty0, stage, phase, C, m, p,
+                                                                   ldc, tm * BM, tn * BN, wm, wn, k0, k1,
+                                                                   ACC || tail, f, lane);
+    if (head) split_signal(flags + blockIdx.x + 1, lane);  // low-k partial of this tile -> next CTA
+    if (tail) split_release(flags + blockIdx.x, 2 * Tr::kConsumerWarps, lane);
   }
 }
 
@@ -377,6 +433,18 @@ bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t col
                    ld);
 }
 
+// Opt in to the full dynamic smem per CTA and the maximum shared-memory carveout:
+// without the carveout the driver picked a smaller L1/smem split and the small
+// tiles fit fewer CTAs per SM than their smem allows (32x32x3: 6 instead of 8).
+template <int BM, int BN, int WM, int WN, int ST, bool ACC>
+cudaError_t k1_attrs() {
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       K1Traits<BM, BN, WM, WN, ST>::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  return e;
+}
+
 template <int BM, int BN, int WM, int WN, int ST>
 int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   using Tr = K1Traits<BM, BN, WM, WN, ST>;
@@ -388,21 +456,25 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(k_dgemm_tma<BM, BN, WM, WN, ST, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(k_dgemm_tma<BM, BN, WM, WN, ST, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+    attr_err = k1_attrs<BM, BN, WM, WN, ST, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true>();
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  unsigned int* ctr = nullptr;
-  static const bool force_static = getenv("MOA_STATIC_TILES") != nullptr;  // A/B knob (profiling only)
-  if (!force_static && plan.tiles > plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
+  // Schedule (see the kernel): stream-K when the last partial wave matters (fewer
+  // than kSkMaxWaves waves), dynamic tiles otherwise, static stride for one wave.
+  unsigned int *flags = nullptr, *ctr = nullptr;
+  if (plan.tiles > plan.grid) {
+    if (use_stream_k(plan.tiles, plan.grid)) {
+      if (!acquire_split_flags((unsigned)plan.grid + 1, &flags)) return MOA_ERR_CUDA;
+    } else if (!acquire_tile_counter(stream, &ctr)) {
+      return MOA_ERR_CUDA;
+    }
+  }
   kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                                       plan.raster_group, ctr);
+                                                       plan.raster_group, flags, ctr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -414,13 +486,17 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
 // The chooser's candidate lifted blocks. ctas_per_sm is refined at first use
 // from the occupancy API (registers are what limit it; see K1Traits). eta is the
 // per-tile efficiency relative to 128x128, measured once at N=16384 where wave
-// quantisation vanishes (profiles/r01_configs.json block_sweep: 0.9838 / 0.9775 /
-// 0.9325 of peak) — a property of the tile config, not a per-shape tuning.
+// quantisation vanishes (tools/small_n.py -> profiles/r01_small_n.json: 0.9806 /
+// 0.9614 / 0.9574 / 0.9665 of peak) — a property of the tile config, not a
+// per-shape tuning. 64x32 is discounted to 0.95: its 4-warp CTAs lose more than
+// that at mid sizes (N=768: 44 vs 31 us for 64x64), so it is picked only where its
+// finer grain decides (N <= 512).
 TileConfig kK1Configs[] = {
     // kernel, bm, bn, bk, stages, threads, ctas/SM, smem, eta
     {MOA_KERNEL_DGEMM_TMA, 128, 128, 16, 6, K1Traits<128, 128, 4, 2, 6>::kThreads, 1, K1Traits<128, 128, 4, 2, 6>::kSmem, 1.00},
-    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 2, 4>::kThreads, 1, K1Traits<128, 64, 4, 2, 4>::kSmem, 0.994},
-    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 4, 4>::kThreads, 2, K1Traits<64, 64, 2, 4, 4>::kSmem, 0.948},
+    {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 2, 4>::kThreads, 1, K1Traits<128, 64, 4, 2, 4>::kSmem, 0.980},
+    {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 4, 4>::kThreads, 2, K1Traits<64, 64, 2, 4, 4>::kSmem, 0.976},
+    {MOA_KERNEL_DGEMM_TMA, 64, 32, 16, 4, K1Traits<64, 32, 2, 2, 4>::kThreads, 4, K1Traits<64, 32, 2, 2, 4>::kSmem, 0.95},
 };
 TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
@@ -430,7 +506,7 @@ template <int BM, int BN, int WM, int WN, int ST>
 int k1_occupancy() {
   using Tr = K1Traits<BM, BN, WM, WN, ST>;
   auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem) != cudaSuccess) return 0;
+  if (k1_attrs<BM, BN, WM, WN, ST, false>() != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Tr::kThreads, Tr::kSmem) != cudaSuccess) return 0;
   return n;
@@ -439,8 +515,9 @@ int k1_occupancy() {
 void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
-    int o[3] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>()};
-    for (int i = 0; i < 3; ++i)
+    int o[4] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
+                k1_occupancy<64, 32, 2, 2, 4>()};
+    for (int i = 0; i < 4; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
@@ -469,6 +546,7 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
   if (plan.bm == 128 && plan.bn == 128 && plan.stages == 6) return launch_k1<128, 128, 4, 2, 6>(plan, g, stream);
   if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 2, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 4, 4>(plan, g, stream);
+  if (plan.bm == 64 && plan.bn == 32 && plan.stages == 4) return launch_k1<64, 32, 2, 2, 4>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }

@@ -194,9 +194,19 @@ bool tma_eligible(const GemmArgs& g, int es) {
          al16(g.A) && al16(g.B) && al16(g.C) && g.m < INT32_MAX && g.n < INT32_MAX && g.p < INT32_MAX;
 }
 
+// Persistent grid. K1 (stream-K, moa_ptx.cuh sk_plan) needs grid <= tiles and all
+// CTAs resident: a whole number of CTAs per SM up to the occupancy, so every SM
+// carries the same share of the balanced work. Other kernels: min(tiles, slots).
+int32_t grid_for(int kernel, int64_t tiles, int sms, int ctas_per_sm) {
+  const int64_t slots = (int64_t)sms * ctas_per_sm;
+  if (kernel != MOA_KERNEL_DGEMM_TMA || tiles < sms || tiles >= slots) return (int32_t)(tiles < slots ? tiles : slots);
+  return (int32_t)((int64_t)sms * (tiles / sms));
+}
+
 // The static chooser: among the compiled tile configs of
 // `kernel`, pick the one with the best predicted SM-level efficiency
-//   eff = (m*p) / (waves * sms * bm*bn) * eta,   waves = ceil(tiles / sms),
+//   eff = (m*p) / (waves * sms * bm*bn) * eta,   waves = ceil(tiles / sms)
+// (for K1 stream-K plans: (m*p) / (tiles * bm*bn) * eta * 0.99, no wave loss),
 // i.e. the lifted block (bm x bn) "as close as possible" to filling every SM's
 // fp64 pipe for a whole number of waves. No measurement, no autotuning.
 int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* out) {
@@ -217,7 +227,11 @@ int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* 
     if (c.smem_bytes > ds.smem_optin) continue;
     const int64_t tm = (m + c.bm - 1) / c.bm, tn = (p + c.bn - 1) / c.bn, tiles = tm * tn;
     const int64_t waves = (tiles + ds.sms - 1) / ds.sms;
-    const double eff = (double)m * (double)p / ((double)waves * ds.sms * (double)c.bm * c.bn) * c.eta;
+    double eff = (double)m * (double)p / ((double)waves * ds.sms * (double)c.bm * c.bn) * c.eta;
+    // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
+    // cut tiles cost a partial store + reload and an extra pipeline fill: -1%.
+    if (c.kernel == MOA_KERNEL_DGEMM_TMA && use_stream_k(tiles, grid_for(c.kernel, tiles, ds.sms, c.ctas_per_sm)))
+      eff = (double)m * (double)p / ((double)tiles * c.bm * c.bn) * c.eta * 0.99;
     if (eff > best + 1e-12) {
       best = eff;
       bi = i;
@@ -235,8 +249,7 @@ int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* 
   out->tiles_m = (m + c.bm - 1) / c.bm;
   out->tiles_n = (p + c.bn - 1) / c.bn;
   out->tiles = out->tiles_m * out->tiles_n;
-  const int64_t slots = (int64_t)ds.sms * c.ctas_per_sm;
-  out->grid = (int32_t)(out->tiles < slots ? out->tiles : slots);
+  out->grid = grid_for(c.kernel, out->tiles, ds.sms, c.ctas_per_sm);
   out->raster_group = (int32_t)(out->tiles_m < 8 ? out->tiles_m : 8);
   if (out->raster_group < 1) out->raster_group = 1;
   out->smem_bytes = c.smem_bytes;
@@ -324,8 +337,7 @@ int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t
         pl.tiles_m = (g.m + pl.bm - 1) / pl.bm;
         pl.tiles_n = (g.p + pl.bn - 1) / pl.bn;
         pl.tiles = pl.tiles_m * pl.tiles_n;
-        const int64_t slots = (int64_t)ds.sms * pl.ctas_per_sm;
-        pl.grid = (int32_t)(pl.tiles < slots ? pl.tiles : slots);
+        pl.grid = grid_for(pl.kernel, pl.tiles, ds.sms, pl.ctas_per_sm);
         if (plan->grid > 0 && plan->grid < pl.grid) pl.grid = plan->grid;
         if (plan->raster_group > 0) pl.raster_group = plan->raster_group;
         found = true;

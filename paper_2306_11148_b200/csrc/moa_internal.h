@@ -56,6 +56,20 @@ struct TileConfig {
   double eta;  // per-tile efficiency prior (smaller tiles: more smem/L2 traffic per flop)
 };
 // Return the number of configs for a kernel id and fill *out (static storage).
+#ifdef __CUDACC__
+#define MOA_HD __host__ __device__
+#else
+#define MOA_HD
+#endif
+// K1 schedule choice (host chooser + launcher): stream-K only while the last partial wave is a large share of
+// the work (measured: stream-K ahead up to N=6144, even at 8192 = 27.7 waves of
+// 128x128, behind at 16384 = 110.7 waves where the dynamic schedule's L2 lockstep
+// wins).
+constexpr int64_t kSkMaxWaves = 20;
+MOA_HD inline bool use_stream_k(int64_t tiles, int64_t grid) {
+  return grid > 0 && tiles > grid && tiles % grid != 0 && tiles < kSkMaxWaves * grid;
+}
+
 int dgemm_tile_configs(int kernel, const TileConfig** out);  // moa_dgemm.cu
 int sgemm_tile_configs(int kernel, const TileConfig** out);  // moa_sgemm.cu
 int tf32_tile_configs(int kernel, const TileConfig** out);   // moa_tf32.cu

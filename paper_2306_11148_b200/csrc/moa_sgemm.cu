@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
       mbar_wait(full0 + 8 * stage, phase);
       const uint8_t* sa = sptr + stage * Tr::kStageBytes;
       ffma_slab(acc, sa, sa + Tr::kABytes, ty, tx);
+      fence_proxy_async_smem();  // LDS reads before the producer's next TMA write (WAR)
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * stage);
       if (++stage == STAGES) {

@@ -86,9 +86,6 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -251,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int64_t tm, tn;
       tile_coords(t, tiles_m, tiles_n, group, tm, tn);
       mbar_wait(acc_full + 8 * ab, aph);
+      __syncwarp();  // reconverge before tcgen05.ld (.sync.aligned)
       tc_fence_after();
       const int64_t row = tm * kBM + row_in_tile;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * Tr::kAccCols);
@@ -442,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
       for (int kt = 0; kt < ktiles; ++kt) {
         mbar_wait(raw_full + 8 * st, ph);  // implies the stage's previous MMAs are done
+        __syncwarp();  // reconverge before tcgen05.st (.sync.aligned)
         uint8_t* sa = sptr + st * Tr::kStageBytes;
         uint32_t big[32], sml[32];
 #pragma unroll
@@ -485,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int64_t tm, tn;
       tile_coords(t, tiles_m, tiles_n, group, tm, tn);
       mbar_wait(acc_full + 8 * ab, aph);
+      __syncwarp();  // reconverge before tcgen05.ld (.sync.aligned)
       tc_fence_after();
       const int64_t row = tm * kBM + row_in_tile;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * BN);

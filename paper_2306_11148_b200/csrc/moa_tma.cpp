@@ -74,4 +74,48 @@ bool acquire_tile_counter(cudaStream_t stream, unsigned int** out) {
   return true;
 }
 
+namespace {
+// Split-tile flags: one uint32 per CTA boundary of a stream-K launch. The ring is
+// zeroed once when created; every flag used by a launch is returned to 0 by its
+// last reader inside that launch, so no per-launch memset is needed. Slots are
+// handed out round-robin, so launches in flight on different streams (up to
+// kFlagSlots / grid of them) never share a flag.
+constexpr unsigned int kFlagSlots = 1u << 18;
+struct FlagPool {
+  unsigned int* dev = nullptr;
+  unsigned int next = 0;
+};
+std::mutex g_flag_mu;
+std::map<int, FlagPool> g_flag;
+}  // namespace
+
+bool acquire_split_flags(unsigned int count, unsigned int** out) {
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
+  unsigned int* slot = nullptr;
+  if (e == cudaSuccess && count > kFlagSlots) {
+    set_error("split flags: grid larger than the flag pool");
+    return false;
+  }
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    FlagPool& pool = g_flag[device];
+    if (!pool.dev) {  // library-owned, once (not inside stream capture: the first GEMM call creates it)
+      e = cudaMalloc(&pool.dev, kFlagSlots * sizeof(unsigned int));
+      if (e == cudaSuccess) e = cudaMemset(pool.dev, 0, kFlagSlots * sizeof(unsigned int));
+    }
+    if (e == cudaSuccess) {
+      if (pool.next + count > kFlagSlots) pool.next = 0;
+      slot = pool.dev + pool.next;
+      pool.next += count;
+    }
+  }
+  if (e != cudaSuccess) {
+    set_error(std::string("split flags: ") + cudaGetErrorString(e));
+    return false;
+  }
+  *out = slot;
+  return true;
+}
+
 }  // namespace moa

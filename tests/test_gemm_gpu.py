@@ -179,6 +179,41 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
         assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
 
 
+K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4)]
+
+
+@pytest.mark.parametrize("shape", [(2000, 200, 2000), (1500, 100, 3000), (2100, 56, 1030)])
+def test_stream_k_split_tiles_bitwise(cuda_device, shape):
+    """Stream-K (moa_ptx.cuh sk_plan): tiles cut along k between two CTAs, the high-k
+    part continuing the chain from the stored low-k partial, are bitwise the fused
+    ip.c result — for every compiled tile config, with ragged k (n % 16 != 0), and in
+    accumulate mode (C := C0 + A.B, chain started from C0)."""
+    import torch
+    moa = _moa()
+    m, n, p = shape
+    A, B = _host(m, n, p, 21)
+    ref = O.ip(A, B, fused=True)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    base = moa.plan(m, n, p)
+    split_seen = False
+    for (bm, bn, st) in K1_CONFIGS:
+        pl = moa.Plan(**{**base.__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
+        out = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+        moa.gemm_with_plan(tA, tB, out, pl)
+        torch.cuda.synchronize()
+        assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
+        tiles = -(-m // bm) * -(-p // bn)
+        split_seen |= tiles >= pl.sms and tiles % pl.sms != 0
+    assert split_seen
+    # accumulate mode: two k-panels through moa_gemm_acc equal the one-call chain
+    k1 = 48
+    C = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+    moa.gemm_acc(tA[:, :k1], tB[:k1], C, accumulate=False)
+    moa.gemm_acc(tA[:, k1:], tB[k1:], C, accumulate=True)
+    torch.cuda.synchronize()
+    assert _bits_equal(C.cpu().numpy(), ref)
+
+
 def test_plan_is_static_and_sane(cuda_device):
     moa = _moa()
     for (m, n, p) in [(256, 256, 256), (1024, 1024, 1024), (8192, 8192, 8192), (16384, 16384, 16384),

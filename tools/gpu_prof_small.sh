@@ -1,4 +1,6 @@
-#!/bin/bash
-mkdir -p gpurun_out
-timeout 900 ncu --set full --clock-control none -k regex:k_dgemm_tma -s 2 -c 4 -o gpurun_out/prof_small python tools/prof_small.py ${1:-2048} > gpurun_out/ncu_small.log 2>&1
-echo "rc=$?"; tail -2 gpurun_out/ncu_small.log
+set -x
+for c in "64 64 4" "32 32 3" "128 64 4"; do
+  t=$(echo $c | tr ' ' _)
+  ncu --set full --clock-control none -k regex:k_dgemm_tma -s 3 -c 1 -o gpurun_out/ncu_n1024_$t python tools/prof_small.py 1024 $c > /dev/null 2>&1
+done
+ls gpurun_out

@@ -1,16 +1,21 @@
-"""Small-N fp64 runs for ncu: each compiled tile config at N (default 2048)."""
-import os, sys
+#!/usr/bin/env python3
+"""One fp64 GEMM at N with tile (bm,bn,stages) after warm-ups, for ncu (-s 3 -c 1)."""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-import paper_2306_11148_b200 as moa
-from inputs import inputs as I
-N = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
-A = torch.empty((N, N), dtype=torch.float64, device="cuda"); B = torch.empty_like(A); C = torch.empty_like(A)
-I.device_fill(A, 1, I.ID_A); I.device_fill(B, 1, I.ID_B)
-base = moa.plan(N, N, N)
-for (bm, bn, st) in [(128, 128, 6), (64, 64, 4)]:
-    q = moa.Plan(**{**base.__dict__, "bm": bm, "bn": bn, "stages": st})
-    for _ in range(3):
-        moa.gemm_with_plan(A, B, C, q)
+import torch  # noqa: E402
+
+import paper_2306_11148_b200 as moa  # noqa: E402
+from inputs import inputs as I  # noqa: E402
+
+N, bm, bn, st = (int(x) for x in sys.argv[1:5])
+A = torch.empty((N, N), dtype=torch.float64, device="cuda")
+B = torch.empty_like(A)
+C = torch.empty_like(A)
+I.device_fill(A, 1, I.ID_A)
+I.device_fill(B, 1, I.ID_B)
+q = moa.Plan(**{**moa.plan(N, N, N).__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
+for _ in range(5):
+    moa.gemm_with_plan(A, B, C, q)
 torch.cuda.synchronize()
-print("ok")
