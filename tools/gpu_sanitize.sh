@@ -1,6 +1,6 @@
 #!/bin/bash
-mkdir -p gpurun_out
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "$tool rc=$?"; tail -4 gpurun_out/sanitize_$tool.log
+mkdir -p gpurun_out/sanitizer
+for t in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_run.py > gpurun_out/sanitizer/r01_$t.log 2>&1
+  echo "$t rc=$?"; tail -3 gpurun_out/sanitizer/r01_$t.log
 done

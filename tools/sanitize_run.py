@@ -1,5 +1,6 @@
 """Small-shape runs of every kernel (K1 fp64 TMA, K2 generic, K3 FFMA, K3g, K4 3xTF32)
-for compute-sanitizer (memcheck / racecheck / synccheck)."""
+for compute-sanitizer (memcheck / racecheck / synccheck), plus K1 in its stream-K
+(2000x48x2000: 256 tiles on 148 CTAs) and dynamic (7040x16x7040: >= 20 waves) schedules."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -15,4 +16,11 @@ for (m, n, p) in [(200, 96, 260), (130, 34, 66)]:
         err = np.linalg.norm(C.cpu().numpy() - O.ip(A, B)) / np.linalg.norm(O.ip(A, B))
         print(m, n, p, dt.__name__, prec, moa.plan(m, n, p, {np.float64: 0, np.float32: 1}[dt] if prec is None else 2).kernel, f"{err:.2e}")
         ok &= err < 5e-3
+for (m, n, p) in [(2000, 48, 2000), (7040, 16, 7040)]:
+    A = I.host_matrix(m, n, 3, I.ID_A); B = I.host_matrix(n, p, 3, I.ID_B)
+    C = moa.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    same = bool(np.all(C == O.ip(A, B, fused=True)))
+    pl = moa.plan(m, n, p)
+    print(m, n, p, "float64 K1", pl.bm, pl.bn, "tiles", pl.tiles, "grid", pl.grid, "bitwise" if same else "MISMATCH")
+    ok &= same
 print("ALL OK" if ok else "MISMATCH")
