@@ -65,7 +65,10 @@ struct TileConfig {
 // the work (measured: stream-K ahead up to N=6144, even at 8192 = 27.7 waves of
 // 128x128, behind at 16384 = 110.7 waves where the dynamic schedule's L2 lockstep
 // wins).
-constexpr int64_t kSkMaxWaves = 20;
+#ifndef MOA_AB_SK_MAX_WAVES  // A/B builds only (tools/build_variant.sh)
+#define MOA_AB_SK_MAX_WAVES 20
+#endif
+constexpr int64_t kSkMaxWaves = MOA_AB_SK_MAX_WAVES;
 MOA_HD inline bool use_stream_k(int64_t tiles, int64_t grid) {
   return grid > 0 && tiles > grid && tiles % grid != 0 && tiles < kSkMaxWaves * grid;
 }

@@ -1,0 +1,7 @@
+#!/bin/bash
+cp paper_2306_11148_b200/libmoa.so /tmp/libmoa_prod.so
+python tools/ab_sk.py > gpurun_out/ab_sk_prod.json 2>/dev/null
+cp ab/libmoa_nosk.so paper_2306_11148_b200/libmoa.so
+python tools/ab_sk.py > gpurun_out/ab_sk_nosk.json 2>/dev/null
+cp /tmp/libmoa_prod.so paper_2306_11148_b200/libmoa.so
+python tools/ab_sk.py > gpurun_out/ab_sk_prod2.json 2>/dev/null
