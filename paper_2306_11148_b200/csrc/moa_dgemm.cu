@@ -210,7 +210,7 @@ struct K1Traits {
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 16 * STAGES + 64;  // + descriptors, sk plan
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 24 * STAGES;  // + piece descriptors
   static_assert(BM == 32 * WARPS_M, "warp tile is 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -251,18 +251,20 @@ __device__ __forceinline__ void consume_piece(Acc<NBOX>& acc, const uint8_t* spt
 // ACC: start every tile's chain from the C in memory (moa_gemm_acc k-panel chains).
 //
 // Work assignment (the producer decides; the consumers only read piece descriptors):
-//  * flags != null — stream-K (moa_ptx.cuh sk_plan): static, balanced runs of
-//    k-slabs; pieces head, data-parallel tiles, whole stream-K tiles, tail. Used
-//    for few waves, where the last partial wave costs most.
-//  * tile_ctr != null — dynamic: whole tiles claimed from an atomic counter. Used
-//    for many waves: claiming keeps all CTAs of a wave in k-lockstep, so they share
-//    the A/B k-slabs in L2 (a static schedule drifts: 53% L2 hits vs 82%, N=16384).
-//  * neither — static stride (tiles <= grid).
-// The producer publishes each piece (tile, k0, k1) in the slot of its first stage,
-// before that stage's full-barrier arrive (release); t = -1 ends the work.
+//  * tile_ctr != null: whole tiles claimed dynamically from an atomic counter and,
+//    when flags != null (the last wave is partial), the stream-K runs of
+//    moa_ptx.cuh sk_run for the last S tiles, one run per CTA, claimed from the
+//    same counter. Claiming keeps all CTAs of a wave in k-lockstep, so they share
+//    the A/B k-slabs in L2 (a fully static schedule drifted: 53% L2 hits vs 82%
+//    at N=16384); the runs remove the partial last wave.
+//  * tile_ctr == null, flags != null: every tile is in the stream-K region
+//    (tiles < 2G): run r = CTA index.
+//  * neither: static stride (tiles <= grid).
+// The producer publishes each piece (tile, k0, k1, run) in the slot of its first
+// stage, before that stage's full-barrier arrive (release); t = -1 ends the work.
 struct PieceDesc {
   int64_t t;
-  int32_t k0, k1;
+  int32_t k0, k1, run, pad;
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC>
@@ -280,7 +282,6 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
   volatile PieceDesc* desc = reinterpret_cast<volatile PieceDesc*>(smem_raw + (empty0 + STAGES * 8 - raw));
-  SkPieces* skq = reinterpret_cast<SkPieces*>(smem_raw + (empty0 + STAGES * 8 + 16 * STAGES - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (int)((n + kBK - 1) / kBK);
 
@@ -291,8 +292,6 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
       mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
     }
     fence_mbar_init();
-    // the stream-K plan is computed here, not by the producer (40 registers there)
-    if (flags) *skq = sk_pieces(tiles_m * tiles_n, ktiles, gridDim.x, blockIdx.x);
   }
   __syncthreads();
 
@@ -304,7 +303,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
       prefetch_tmap(&tmB);
       int stage = 0;
       uint32_t phase = 0;
-      auto emit = [&](int64_t t, int k0, int k1) {
+      auto emit = [&](int64_t t, int k0, int k1, int run) {
         int64_t tm, tn;
         tile_coords(t, tiles_m, tiles_n, group, tm, tn);
         const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
@@ -314,6 +313,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
             desc[stage].t = t;
             desc[stage].k0 = k0;
             desc[stage].k1 = k1;
+            desc[stage].run = run;
           }
           const uint32_t fb = full0 + 8 * stage;
           mbar_arrive_expect_tx(fb, Tr::kStageBytes);
@@ -329,16 +329,33 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
         }
       };
       const int64_t tiles = tiles_m * tiles_n;
-      if (flags) {
-        const int64_t np = skq->npieces;
-        for (int64_t i = 0; i < np; ++i) {
-          const Piece pc = piece_at(skq, i, ktiles, gridDim.x, blockIdx.x);
-          emit(pc.t, pc.k0, pc.k1);
+      if (flags && !tile_ctr) {
+        // every tile is in the stream-K region (tiles < 2G): run = CTA index, no
+        // claiming (claiming cost ~4 us at N=1024 where the kernel lasts ~70 us)
+        const SkRun q = sk_run(tiles, ktiles, gridDim.x, blockIdx.x);
+        const int r = (int)blockIdx.x;
+        if (q.hk > 0) emit(q.hb, 0, q.hk, r);
+        for (int64_t w = q.f0; w < q.f1; ++w) emit(w, 0, ktiles, r);
+        if (q.tk > 0) emit(q.ta, q.tk, ktiles, r);
+      } else if (tile_ctr) {
+        const int64_t G = gridDim.x, first = flags ? sk_first_tile(tiles, G) : tiles;
+        for (;;) {
+          const int64_t t = (int64_t)atomicAdd(tile_ctr, 1u);
+          if (t < first) {
+            emit(t, 0, ktiles, -1);
+            continue;
+          }
+          const int64_t r = t - first;  // this CTA's stream-K run (at most one)
+          if (flags && r < G) {
+            const SkRun q = sk_run(tiles, ktiles, G, r);
+            if (q.hk > 0) emit(q.hb, 0, q.hk, (int)r);
+            for (int64_t w = q.f0; w < q.f1; ++w) emit(w, 0, ktiles, (int)r);
+            if (q.tk > 0) emit(q.ta, q.tk, ktiles, (int)r);
+          }
+          break;
         }
       } else {
-        for (int64_t t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : (int64_t)blockIdx.x; t < tiles;
-             t = tile_ctr ? (int64_t)atomicAdd(tile_ctr, 1u) : t + gridDim.x)
-          emit(t, 0, ktiles);
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) emit(t, 0, ktiles, -1);
       }
       mbar_wait(empty0 + 8 * stage, phase ^ 1u);  // end-of-work sentinel slot
       desc[stage].t = -1;
@@ -366,16 +383,16 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     __syncwarp();
     const int64_t t = desc[stage].t;
     if (t < 0) break;
-    const int k0 = desc[stage].k0, k1 = desc[stage].k1;
+    const int k0 = desc[stage].k0, k1 = desc[stage].k1, run = desc[stage].run;
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
-    if (tail) split_wait(flags + blockIdx.x, Tr::kConsumerWarps, lane);
+    if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     consume_piece<Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(acc, sptr, full0, empty0, stage, phase, C, m, p,
                                                                    ldc, tm * BM, tn * BN, wm, wn, k0, k1,
                                                                    ACC || tail, f, lane);
-    if (head) split_signal(flags + blockIdx.x + 1, lane);  // low-k partial of this tile -> next CTA
-    if (tail) split_release(flags + blockIdx.x, 2 * Tr::kConsumerWarps, lane);
+    if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
+    if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
   }
 }
 
@@ -463,15 +480,14 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  // Schedule (see the kernel): stream-K when the last partial wave matters (fewer
-  // than kSkMaxWaves waves), dynamic tiles otherwise, static stride for one wave.
+  // Schedule (see the kernel): dynamic tiles, plus stream-K runs when the last
+  // wave is partial; static stride for one wave.
   unsigned int *flags = nullptr, *ctr = nullptr;
   if (plan.tiles > plan.grid) {
-    if (use_stream_k(plan.tiles, plan.grid)) {
-      if (!acquire_split_flags((unsigned)plan.grid + 1, &flags)) return MOA_ERR_CUDA;
-    } else if (!acquire_tile_counter(stream, &ctr)) {
-      return MOA_ERR_CUDA;
-    }
+    const bool sk = use_stream_k(plan.tiles, plan.grid);
+    if (sk && !acquire_split_flags((unsigned)plan.grid + 1, &flags)) return MOA_ERR_CUDA;
+    // no counter when every tile is a stream-K run (tiles < 2G: run = CTA index)
+    if (!(sk && sk_first_tile(plan.tiles, plan.grid) == 0) && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   }
   kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
                                                        plan.raster_group, flags, ctr);

@@ -194,7 +194,7 @@ bool tma_eligible(const GemmArgs& g, int es) {
          al16(g.A) && al16(g.B) && al16(g.C) && g.m < INT32_MAX && g.n < INT32_MAX && g.p < INT32_MAX;
 }
 
-// Persistent grid. K1 (stream-K, moa_ptx.cuh sk_plan) needs grid <= tiles and all
+// Persistent grid. K1 (stream-K runs, moa_ptx.cuh sk_run) needs grid <= tiles and all
 // CTAs resident: a whole number of CTAs per SM up to the occupancy, so every SM
 // carries the same share of the balanced work. Other kernels: min(tiles, slots).
 int32_t grid_for(int kernel, int64_t tiles, int sms, int ctas_per_sm) {

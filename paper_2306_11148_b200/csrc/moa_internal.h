@@ -61,16 +61,10 @@ struct TileConfig {
 #else
 #define MOA_HD
 #endif
-// K1 schedule choice (host chooser + launcher): stream-K only while the last partial wave is a large share of
-// the work (measured: stream-K ahead up to N=6144, even at 8192 = 27.7 waves of
-// 128x128, behind at 16384 = 110.7 waves where the dynamic schedule's L2 lockstep
-// wins).
-#ifndef MOA_AB_SK_MAX_WAVES  // A/B builds only (tools/build_variant.sh)
-#define MOA_AB_SK_MAX_WAVES 20
-#endif
-constexpr int64_t kSkMaxWaves = MOA_AB_SK_MAX_WAVES;
+// K1 schedule choice (host chooser + launcher): the stream-K runs are used
+// whenever the last wave is partial (moa_ptx.cuh sk_first_tile / sk_run).
 MOA_HD inline bool use_stream_k(int64_t tiles, int64_t grid) {
-  return grid > 0 && tiles > grid && tiles % grid != 0 && tiles < kSkMaxWaves * grid;
+  return grid > 0 && tiles > grid && tiles % grid != 0;
 }
 
 int dgemm_tile_configs(int kernel, const TileConfig** out);  // moa_dgemm.cu

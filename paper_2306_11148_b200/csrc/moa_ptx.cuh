@@ -61,66 +61,43 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 // ------------------------- stream-K schedule (K1) -----------------------------
-// Static, balanced assignment of the (tile, k-slab) work of one launch to its G
-// persistent CTAs. Full waves are data-parallel (CTA c takes tiles c, c+G, ...);
-// the last S tiles (remainder + one wave, S in [G, 2G)) are cut into G equal runs
-// of k-slabs. A tile cut between CTAs c and c+1 has its low-k part ("head") at
-// the end of c's run and its high-k part ("tail") at the start of c+1's run.
-// Bitwise rule: the high-k part continues the fma chain from the stored low-k
-// partial (DMMA/FFMA continue the chain from their C operand), so the result
-// equals the unsplit tile. Within its stream-K run each CTA computes its head
-// FIRST and its tail LAST: with runs R >= K slabs, c+1 reaches its tail after
-// h_{c+1} + F = R - K + h_c >= h_c slabs, i.e. never before c has finished the
-// head it depends on.
-struct SkPlan {
-  int64_t dp_waves;  // full data-parallel waves per CTA
-  int64_t sk_first;  // first stream-K tile (= dp_waves * G)
-  int64_t u0, u1;    // this CTA's run of stream-K units [u0, u1), unit = one k-slab
-};
-__device__ __forceinline__ SkPlan sk_plan(int64_t tiles, int64_t ktiles, int64_t G, int64_t c) {
-  SkPlan s;
-  s.dp_waves = (tiles % G == 0) ? tiles / G : (tiles >= 2 * G ? tiles / G - 1 : 0);
-  s.sk_first = s.dp_waves * G;
-  const int64_t U = (tiles - s.sk_first) * ktiles;
-  s.u0 = U * c / G;
-  s.u1 = U * (c + 1) / G;
-  return s;
+// Balanced assignment of the (tile, k-slab) work of one launch to its G persistent
+// CTAs. The first D = (T/G - 1)*G tiles (full waves but one) are data-parallel and
+// claimed dynamically from the launch's tile counter. The last S = T - D tiles
+// (S in [G, 2G)) are cut into G equal runs of k-slabs; when a CTA's claim runs
+// past D, the value it drew minus D is its run index r. A tile cut between runs
+// r and r+1 has its low-k part ("head") at the end of run r and its high-k part
+// ("tail") at the start of run r+1.
+// Bitwise rule: the tail continues the fma chain from the stored low-k partial
+// (DMMA/FFMA continue the chain from their C operand), so the result equals the
+// unsplit tile. Within its run a CTA computes its head FIRST and its tail LAST.
+// Runs are claimed in counter order, so run r-1 was claimed no later than run r,
+// and with runs R >= K slabs run r reaches its tail after h_r + F_r = R - K +
+// h_{r-1} >= h_{r-1} slabs of its own: never before run r-1's head is done (in the
+// uniform-speed model; otherwise it waits on the flag, and there is no cycle:
+// run 0 has no tail).
+// Dynamic claiming of the data-parallel tiles keeps all CTAs of a wave in
+// k-lockstep (they share the A/B k-slabs in L2) and absorbs SM speed variance; the
+// runs remove the last partial wave.
+__host__ __device__ __forceinline__ int64_t sk_first_tile(int64_t tiles, int64_t G) {
+  return tiles >= 2 * G ? (tiles / G - 1) * G : 0;
 }
-// The pieces of one CTA's stream-K schedule in processing order: head (tile hb,
-// k [0, hk)), the data-parallel tiles cta + w*G, the whole stream-K tiles
-// [f0, f1), tail (tile ta, k [tk, K)). Head first measured faster than
-// data-parallel first (3.80 vs 3.91 ms at N=4096): with few waves the cold start
-// dominates, and at the end every CTA runs only its tail.
-struct SkPieces {
-  int64_t hb, ta, f0, dp_waves, npieces;
-  int32_t hk, tk;
+struct SkRun {
+  int64_t hb, ta, f0, f1;  // head tile, tail tile, whole tiles [f0, f1)
+  int32_t hk, tk;          // head k-slabs [0, hk), tail k-slabs [tk, K)
 };
-struct Piece {
-  int64_t t;
-  int k0, k1;
-};
-__device__ __forceinline__ SkPieces sk_pieces(int64_t tiles, int64_t ktiles, int64_t G, int64_t c) {
-  const SkPlan sk = sk_plan(tiles, ktiles, G, c);
-  SkPieces q;
-  q.hb = sk.sk_first + sk.u1 / ktiles;
-  q.hk = (int32_t)(sk.u1 % ktiles);
-  q.ta = sk.sk_first + sk.u0 / ktiles;
-  q.tk = (int32_t)(sk.u0 % ktiles);
-  q.f0 = sk.sk_first + (sk.u0 + ktiles - 1) / ktiles;
-  const int64_t f1 = sk.sk_first + sk.u1 / ktiles;
-  q.dp_waves = sk.dp_waves;
-  q.npieces = (q.hk > 0) + sk.dp_waves + (f1 - q.f0) + (q.tk > 0);
+__device__ __forceinline__ SkRun sk_run(int64_t tiles, int64_t ktiles, int64_t G, int64_t r) {
+  const int64_t first = sk_first_tile(tiles, G);
+  const int64_t U = (tiles - first) * ktiles;
+  const int64_t u0 = U * r / G, u1 = U * (r + 1) / G;
+  SkRun q;
+  q.hb = first + u1 / ktiles;
+  q.hk = (int32_t)(u1 % ktiles);
+  q.ta = first + u0 / ktiles;
+  q.tk = (int32_t)(u0 % ktiles);
+  q.f0 = first + (u0 + ktiles - 1) / ktiles;
+  q.f1 = first + u1 / ktiles;
   return q;
-}
-__device__ __forceinline__ Piece piece_at(const SkPieces* q, int64_t i, int ktiles, int64_t G, int64_t c) {
-  const int64_t nh = q->hk > 0 ? 1 : 0, dpw = q->dp_waves;
-  const bool head = i < nh, tail = q->tk > 0 && i == q->npieces - 1;
-  const int64_t j = i - nh;
-  Piece pc;
-  pc.t = head ? q->hb : (tail ? q->ta : (j < dpw ? c + j * G : q->f0 + (j - dpw)));
-  pc.k0 = tail ? q->tk : 0;
-  pc.k1 = head ? q->hk : (int)ktiles;
-  return pc;
 }
 
 // Split-tile flag protocol (one flag per CTA boundary; W = consumer warps):
