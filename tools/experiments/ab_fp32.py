@@ -1,21 +1,21 @@
-"""A/B timing of two libmoa.so builds in one process-free way: each run in a subprocess."""
-import os, subprocess, sys, json
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+"""A/B timing of fp32 exact GEMM (K3) between libmoa builds, each in its own subprocess."""
+import os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 code = r'''
-import sys, os, json, ctypes
+import sys, json, ctypes
 sys.path.insert(0, %r)
 import torch
 lib = ctypes.CDLL(%r)
 lib.moa_gemm.argtypes = [ctypes.c_int64]*3 + [ctypes.c_void_p]*3 + [ctypes.c_int, ctypes.c_void_p]
 from inputs import inputs as I
 res = {}
-for N in (4096, 16384):
-    A = torch.empty((N, N), dtype=torch.float64, device="cuda"); B = torch.empty_like(A); C = torch.empty_like(A)
+for N in (8192, 16384):
+    A = torch.empty((N, N), dtype=torch.float32, device="cuda"); B = torch.empty_like(A); C = torch.empty_like(A)
     I.device_fill(A, 1, I.ID_A); I.device_fill(B, 1, I.ID_B)
-    f = lambda: lib.moa_gemm(N, N, N, A.data_ptr(), B.data_ptr(), C.data_ptr(), 0, None)
-    for _ in range(3): f()
+    f = lambda: lib.moa_gemm(N, N, N, A.data_ptr(), B.data_ptr(), C.data_ptr(), 1, None)
+    for _ in range(2): f()
     torch.cuda.synchronize()
-    reps = 40 if N == 4096 else 4
+    reps = 10 if N == 8192 else 3
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps): f()

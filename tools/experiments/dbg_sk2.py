@@ -4,7 +4,7 @@ equals the wrong value (identifies stale/overwritten partials)."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
 import paper_2306_11148_b200 as moa  # noqa: E402

@@ -1,6 +1,6 @@
 """Grid-size experiment for the static tile schedule at small N."""
 import os, sys, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2306_11148_b200 as moa
 from inputs import inputs as I

@@ -1,6 +1,6 @@
 """Eager vs CUDA-graph-replayed timing of small GEMMs (is configs[0] launch-bound?)."""
 import os, sys, json, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2306_11148_b200 as moa
 from inputs import inputs as I

@@ -1,6 +1,6 @@
 """Short fp32 run for ncu: one exact FFMA and one 3xTF32 GEMM at N=8192 (after warm-up)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2306_11148_b200 as moa
 from inputs import inputs as I
