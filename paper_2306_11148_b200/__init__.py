@@ -180,10 +180,22 @@ def _dtype_code(t) -> int:
     raise TypeError(f"unsupported dtype {t.dtype} (float64 or float32)")
 
 
-def _stream_ptr(stream) -> int:
+_raw_stream = None
+
+
+def _stream_ptr(stream, device_index=None) -> int:
+    """Raw cudaStream_t of ``stream`` or of the current stream. The current stream is
+    read with torch's raw getter when present (building a torch Stream object per
+    call cost ~2 us of host time, tools/host_overhead.py)."""
+    global _raw_stream
+    if stream is not None:
+        return stream.cuda_stream
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if _raw_stream is None:
+        _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+    if _raw_stream:
+        return _raw_stream(torch.cuda.current_device() if device_index is None else device_index)
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _mat_check(A, B, out):
@@ -215,7 +227,7 @@ def gemm(A, B, out=None, *, precision: Optional[str] = None, stream=None):
             raise TypeError("3xtf32 needs float32 operands")
         code = F32_3XTF32
     _check(_moa_gemm(m, n, p, A.data_ptr() or None, B.data_ptr() or None, out.data_ptr() or None, code,
-                     _stream_ptr(stream)), "moa_gemm")
+                     _stream_ptr(stream, A.get_device())), "moa_gemm")
     return out
 
 
@@ -228,7 +240,7 @@ def gemm_with_plan(A, B, out, plan_: Plan, *, precision: Optional[str] = None, s
         code = F32_3XTF32
     pt = plan_._to()
     _check(_moa_gemm_with_plan(m, n, p, A.data_ptr() or None, B.data_ptr() or None, out.data_ptr() or None, code,
-                               ctypes.byref(pt), _stream_ptr(stream)), "moa_gemm_with_plan")
+                               ctypes.byref(pt), _stream_ptr(stream, A.get_device())), "moa_gemm_with_plan")
     return out
 
 

@@ -93,36 +93,36 @@ __device__ __forceinline__ FragOffsets make_offsets(int lane) {
   return f;
 }
 
-template <int NBOX>
+template <int MA, int NBOX>
 struct Acc {
-  double v[4][NBOX][2][2];  // [A atom][box][even/odd atom][C pair]
+  double v[MA][NBOX][2][2];  // [A atom][box][even/odd atom][C pair]
 };
 
-template <int NBOX>
-__device__ __forceinline__ void acc_zero(Acc<NBOX>& c) {
+template <int MA, int NBOX>
+__device__ __forceinline__ void acc_zero(Acc<MA, NBOX>& c) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < MA; ++a)
 #pragma unroll
     for (int b = 0; b < NBOX; ++b)
 #pragma unroll
       for (int h = 0; h < 2; ++h) c.v[a][b][h][0] = c.v[a][b][h][1] = 0.0;
 }
 
-// One 16-wide k-slab: 4 k-steps (ascending) x (4 x 2*NBOX) DMMA atoms.
-// a_base: this warp's 32 rows of the A stage; b_base: its first B box.
-template <int NBOX>
-__device__ __forceinline__ void mma_slab(Acc<NBOX>& c, const uint8_t* a_base, const uint8_t* b_base,
+// One 16-wide k-slab: 4 k-steps (ascending) x (MA x 2*NBOX) DMMA atoms.
+// a_base: this warp's 8*MA rows of the A stage; b_base: its first B box.
+template <int MA, int NBOX>
+__device__ __forceinline__ void mma_slab(Acc<MA, NBOX>& c, const uint8_t* a_base, const uint8_t* b_base,
                                          const FragOffsets& f) {
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    double af[4];
+    double af[MA];
     double2 bf[NBOX];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) af[a] = lds64(a_base, a * 8 * kRowBytes + f.a[s]);
+    for (int a = 0; a < MA; ++a) af[a] = lds64(a_base, a * 8 * kRowBytes + f.a[s]);
 #pragma unroll
     for (int b = 0; b < NBOX; ++b) bf[b] = lds128(b_base, b * kBoxBytes + s * 4 * kRowBytes + f.b[s & 1]);
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < MA; ++a)
 #pragma unroll
       for (int b = 0; b < NBOX; ++b) {
         dmma(c.v[a][b][0], af[a], bf[b].x);
@@ -131,17 +131,17 @@ __device__ __forceinline__ void mma_slab(Acc<NBOX>& c, const uint8_t* a_base, co
   }
 }
 
-// Write the warp's 32 x (16*NBOX) block of C. Lane holds, for atom a and box b,
+// Write the warp's 8*MA x (16*NBOX) block of C. Lane holds, for atom a and box b,
 // row rho(g) and columns {2t, 2t+1} (pair 0) and {2t+8, 2t+9} (pair 1).
 // Accumulate mode ("the addition loop to add up the blocks", across
 // launches): start the chain from the C already in memory instead of +0. Because
 // DMMA continues an fma chain from its C operand, a sequence of k-panel launches
 // reproduces the single-launch result bit for bit. Same fragment map as store_acc.
-template <int NBOX, bool kVec>
-__device__ __forceinline__ void load_acc(Acc<NBOX>& c, const double* __restrict__ C, int64_t m, int64_t p,
+template <int MA, int NBOX, bool kVec>
+__device__ __forceinline__ void load_acc(Acc<MA, NBOX>& c, const double* __restrict__ C, int64_t m, int64_t p,
                                          int64_t ldc, int64_t row0, int64_t col0, const FragOffsets& f) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
+  for (int a = 0; a < MA; ++a) {
     const int64_t r = row0 + a * 8 + f.rr;
     const double* crow = C + r * ldc;
 #pragma unroll
@@ -163,11 +163,11 @@ __device__ __forceinline__ void load_acc(Acc<NBOX>& c, const double* __restrict_
   }
 }
 
-template <int NBOX, bool kVec>
-__device__ __forceinline__ void store_acc(const Acc<NBOX>& c, double* __restrict__ C, int64_t m, int64_t p,
+template <int MA, int NBOX, bool kVec>
+__device__ __forceinline__ void store_acc(const Acc<MA, NBOX>& c, double* __restrict__ C, int64_t m, int64_t p,
                                           int64_t ldc, int64_t row0, int64_t col0, const FragOffsets& f) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
+  for (int a = 0; a < MA; ++a) {
     const int64_t r = row0 + a * 8 + f.rr;
     if (r >= m) continue;
     double* crow = C + r * ldc;
@@ -200,18 +200,21 @@ struct K1Traits {
   static constexpr int kNBoxW = BN / WARPS_N / 16;
   // Only the 32x64 warp tile (64 accumulators) needs the producer's registers.
   static constexpr int kProducerWarps = (kConsumerWarps >= 8 && kNBoxW == 4) ? 4 : 1;
-  static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : 2;  // 32x16 warp tiles fit 2 CTAs/SM
+  // 32x16 warp tiles fit 2 CTAs/SM; the 1-2 warp latency tiles (<= 16 rows per
+  // warp) are meant to pack many CTAs per SM
+  static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : (BM / WARPS_M <= 16 ? 8 : 2);
   static constexpr bool kSetMaxNReg = kProducerWarps == 4;
   static constexpr int kProducerRegs = 40;
   static constexpr int kConsumerRegs = 232;
   static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
   static_assert(!kSetMaxNReg || (kProducerRegs + 2 * kConsumerRegs) * 32 <= 16384, "per-SMSP register budget");
   static constexpr int kNBox = BN / WARPS_N / 16;
+  static constexpr int kMA = BM / WARPS_M / 8;  // A atoms (8 rows each) per warp
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 24 * STAGES;  // + piece descriptors
-  static_assert(BM == 32 * WARPS_M, "warp tile is 32 rows");
+  static_assert(BM == 8 * kMA * WARPS_M && (kMA == 1 || kMA == 2 || kMA == 4), "warp tile is 8, 16 or 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
 
@@ -220,16 +223,16 @@ struct K1Traits {
 // low-k partial of a split tile), else from +0: the loads are predicated off by
 // passing m = 0, so there is ONE copy of the slab loop in the kernel (a branch
 // between load_acc and acc_zero once cost 5.4% in register copies).
-template <int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
-__device__ __forceinline__ void consume_piece(Acc<NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
+template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
+__device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
                                               int& stage, uint32_t& phase, double* __restrict__ C, int64_t m,
                                               int64_t p, int64_t ldc, int64_t row0, int64_t col0, int wm, int wn,
                                               int k0, int k1, bool load, const FragOffsets& f, int lane) {
-  load_acc<NBOX, true>(acc, C, load ? m : 0, p, ldc, row0 + wm * 32, col0 + wn * NBOX * 16, f);
+  load_acc<MA, NBOX, true>(acc, C, load ? m : 0, p, ldc, row0 + wm * 8 * MA, col0 + wn * NBOX * 16, f);
   for (int kt = k0; kt < k1; ++kt) {
     mbar_wait(full0 + 8 * stage, phase);  // (ptxas reconverges the spin with BSSY/BSYNC before the DMMAs)
     const uint8_t* sa = sptr + stage * STAGE_BYTES;
-    mma_slab(acc, sa + wm * 32 * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
+    mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
     // WAR across proxies: these generic-proxy LDS reads must be ordered before the
     // producer's next TMA (async-proxy) write of this stage. The arrive's .release
     // alone does not do it (ptxas even hoists the arrive above the slab's last
@@ -245,7 +248,7 @@ __device__ __forceinline__ void consume_piece(Acc<NBOX>& acc, const uint8_t* spt
       phase ^= 1u;
     }
   }
-  store_acc<NBOX, true>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * NBOX * 16, f);
+  store_acc<MA, NBOX, true>(acc, C, m, p, ldc, row0 + wm * 8 * MA, col0 + wn * NBOX * 16, f);
 }
 
 // ACC: start every tile's chain from the C in memory (moa_gemm_acc k-panel chains).
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
 #pragma unroll
   for (int s = 0; s < 4; ++s) asm volatile("" : "+r"(f.a[s]));
   asm volatile("" : "+r"(f.b[0]), "+r"(f.b[1]));
-  Acc<Tr::kNBox> acc;
+  Acc<Tr::kMA, Tr::kNBox> acc;
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
-    consume_piece<Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(acc, sptr, full0, empty0, stage, phase, C, m, p,
+    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(acc, sptr, full0, empty0, stage, phase, C, m, p,
                                                                    ldc, tm * BM, tn * BN, wm, wn, k0, k1,
                                                                    ACC || tail, f, lane);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
@@ -413,13 +416,13 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const FragOffsets f = make_offsets(lane);
   const int64_t tiles = tiles_m * tiles_n;
-  Acc<kNBox> acc;
+  Acc<4, kNBox> acc;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     int64_t tm, tn;
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const int64_t row0 = tm * BM, col0 = tn * BN;
     if (accumulate)
-      load_acc<kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
+      load_acc<4, kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
     else
       acc_zero(acc);
     for (int64_t k0 = 0; k0 < n; k0 += kBK) {
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
       __syncthreads();
       mma_slab(acc, sa + wm * 32 * kRowBytes, sb + wn * kNBox * kBoxBytes, f);
     }
-    store_acc<kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
+    store_acc<4, kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
   }
 }
 
@@ -504,15 +507,21 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
 // per-tile efficiency relative to 128x128, measured once at N=16384 where wave
 // quantisation vanishes (tools/small_n.py -> profiles/r01_small_n.json: 0.9806 /
 // 0.9614 / 0.9574 / 0.9665 of peak) — a property of the tile config, not a
-// per-shape tuning. 64x32 is discounted to 0.95: its 4-warp CTAs lose more than
-// that at mid sizes (N=768: 44 vs 31 us for 64x64), so it is picked only where its
-// finer grain decides (N <= 512).
+// per-shape tuning. 64x32 (4-warp CTAs) is compiled for the block-size experiment
+// but not offered to the chooser (eta 0): with one CTA per SM it leaves one warp per
+// sub-partition and is erratic (N=768: 44 vs 31 us for 64x64; N=640: 28.7 vs 26.8),
+// and the latency tiles below cover the sizes where its finer grain helped.
 TileConfig kK1Configs[] = {
     // kernel, bm, bn, bk, stages, threads, ctas/SM, smem, eta
     {MOA_KERNEL_DGEMM_TMA, 128, 128, 16, 6, K1Traits<128, 128, 4, 2, 6>::kThreads, 1, K1Traits<128, 128, 4, 2, 6>::kSmem, 1.00},
     {MOA_KERNEL_DGEMM_TMA, 128, 64, 16, 4, K1Traits<128, 64, 4, 2, 4>::kThreads, 1, K1Traits<128, 64, 4, 2, 4>::kSmem, 0.980},
     {MOA_KERNEL_DGEMM_TMA, 64, 64, 16, 4, K1Traits<64, 64, 2, 4, 4>::kThreads, 2, K1Traits<64, 64, 2, 4, 4>::kSmem, 0.976},
-    {MOA_KERNEL_DGEMM_TMA, 64, 32, 16, 4, K1Traits<64, 32, 2, 2, 4>::kThreads, 4, K1Traits<64, 32, 2, 2, 4>::kSmem, 0.95},
+    {MOA_KERNEL_DGEMM_TMA, 64, 32, 16, 4, K1Traits<64, 32, 2, 2, 4>::kThreads, 4, K1Traits<64, 32, 2, 2, 4>::kSmem, 0.0},
+    // latency tiles (16x16 outputs per warp): eta here is the latency-regime factor;
+    // the chooser considers them only for tiny problems (moa_host.cpp choose()).
+    // 16x32 first: it wins the ties (N=512: 13.2 vs 22.3 us for 16x16).
+    {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 4, K1Traits<16, 32, 1, 2, 4>::kThreads, 8, K1Traits<16, 32, 1, 2, 4>::kSmem, 1.0},
+    {MOA_KERNEL_DGEMM_TMA, 16, 16, 16, 4, K1Traits<16, 16, 1, 1, 4>::kThreads, 8, K1Traits<16, 16, 1, 1, 4>::kSmem, 1.0},
 };
 TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
@@ -531,9 +540,9 @@ int k1_occupancy() {
 void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
-    int o[4] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
-                k1_occupancy<64, 32, 2, 2, 4>()};
-    for (int i = 0; i < 4; ++i)
+    int o[6] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
+                k1_occupancy<64, 32, 2, 2, 4>(), k1_occupancy<16, 32, 1, 2, 4>(), k1_occupancy<16, 16, 1, 1, 4>()};
+    for (int i = 0; i < 6; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
@@ -563,6 +572,8 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
   if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 2, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 4, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 32 && plan.stages == 4) return launch_k1<64, 32, 2, 2, 4>(plan, g, stream);
+  if (plan.bm == 16 && plan.bn == 32 && plan.stages == 4) return launch_k1<16, 32, 1, 2, 4>(plan, g, stream);
+  if (plan.bm == 16 && plan.bn == 16 && plan.stages == 4) return launch_k1<16, 16, 1, 1, 4>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }

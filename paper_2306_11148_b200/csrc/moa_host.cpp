@@ -197,16 +197,19 @@ bool tma_eligible(const GemmArgs& g, int es) {
 // Persistent grid. K1 (stream-K runs, moa_ptx.cuh sk_run) needs grid <= tiles and all
 // CTAs resident: a whole number of CTAs per SM up to the occupancy, so every SM
 // carries the same share of the balanced work. Other kernels: min(tiles, slots).
-int32_t grid_for(int kernel, int64_t tiles, int sms, int ctas_per_sm) {
+int32_t grid_for(int kernel, int64_t tiles, int sms, int ctas_per_sm, int64_t tile_area) {
   const int64_t slots = (int64_t)sms * ctas_per_sm;
-  if (kernel != MOA_KERNEL_DGEMM_TMA || tiles < sms || tiles >= slots) return (int32_t)(tiles < slots ? tiles : slots);
+  // latency tiles (<= 32x32 outputs, 1-2 warps): one resident CTA per tile
+  if (kernel != MOA_KERNEL_DGEMM_TMA || tiles < sms || tiles >= slots || tile_area <= 32 * 32)
+    return (int32_t)(tiles < slots ? tiles : slots);
   return (int32_t)((int64_t)sms * (tiles / sms));
 }
 
 // The static chooser: among the compiled tile configs of
 // `kernel`, pick the one with the best predicted SM-level efficiency
 //   eff = (m*p) / (waves * sms * bm*bn) * eta,   waves = ceil(tiles / sms)
-// (for K1 stream-K plans: (m*p) / (tiles * bm*bn) * eta * 0.99, no wave loss),
+// (for K1 stream-K plans: (m*p) / (tiles * bm*bn) * eta * 0.99, no wave loss;
+// for the K1 latency tiles, tiny problems only: the longest chain per SM sub-partition),
 // i.e. the lifted block (bm x bn) "as close as possible" to filling every SM's
 // fp64 pipe for a whole number of waves. No measurement, no autotuning.
 int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* out) {
@@ -228,9 +231,17 @@ int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* 
     const int64_t tm = (m + c.bm - 1) / c.bm, tn = (p + c.bn - 1) / c.bn, tiles = tm * tn;
     const int64_t waves = (tiles + ds.sms - 1) / ds.sms;
     double eff = (double)m * (double)p / ((double)waves * ds.sms * (double)c.bm * c.bn) * c.eta;
+    if (c.kernel == MOA_KERNEL_DGEMM_TMA && (int64_t)c.bm * c.bn <= 32 * 32) {
+      // Latency tiles (16x16 outputs per warp, one resident CTA per tile): only for
+      // tiny problems (fewer 64x32 tiles than SMs), where the time is the longest
+      // DMMA chain per SM sub-partition: ceil(warps / (4 SMs)) warps of 16x16 each.
+      if ((double)m * (double)p >= (double)ds.sms * 64.0 * 32.0) continue;
+      const int64_t warps = tiles * ((int64_t)c.bm * c.bn / 256), smsp = 4LL * ds.sms;
+      eff = (double)m * (double)p / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * c.eta;
+    }
     // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
     // cut tiles cost a partial store + reload and an extra pipeline fill: -1%.
-    if (c.kernel == MOA_KERNEL_DGEMM_TMA && use_stream_k(tiles, grid_for(c.kernel, tiles, ds.sms, c.ctas_per_sm)))
+    if (c.kernel == MOA_KERNEL_DGEMM_TMA && use_stream_k(tiles, grid_for(c.kernel, tiles, ds.sms, c.ctas_per_sm, (int64_t)c.bm * c.bn)))
       eff = (double)m * (double)p / ((double)tiles * c.bm * c.bn) * c.eta * 0.99;
     if (eff > best + 1e-12) {
       best = eff;
@@ -249,7 +260,7 @@ int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* 
   out->tiles_m = (m + c.bm - 1) / c.bm;
   out->tiles_n = (p + c.bn - 1) / c.bn;
   out->tiles = out->tiles_m * out->tiles_n;
-  out->grid = grid_for(c.kernel, out->tiles, ds.sms, c.ctas_per_sm);
+  out->grid = grid_for(c.kernel, out->tiles, ds.sms, c.ctas_per_sm, (int64_t)c.bm * c.bn);
   out->raster_group = (int32_t)(out->tiles_m < 8 ? out->tiles_m : 8);
   if (out->raster_group < 1) out->raster_group = 1;
   out->smem_bytes = c.smem_bytes;
@@ -337,7 +348,7 @@ int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t
         pl.tiles_m = (g.m + pl.bm - 1) / pl.bm;
         pl.tiles_n = (g.p + pl.bn - 1) / pl.bn;
         pl.tiles = pl.tiles_m * pl.tiles_n;
-        pl.grid = grid_for(pl.kernel, pl.tiles, ds.sms, pl.ctas_per_sm);
+        pl.grid = grid_for(pl.kernel, pl.tiles, ds.sms, pl.ctas_per_sm, (int64_t)pl.bm * pl.bn);
         if (plan->grid > 0 && plan->grid < pl.grid) pl.grid = plan->grid;
         if (plan->raster_group > 0) pl.raster_group = plan->raster_group;
         found = true;

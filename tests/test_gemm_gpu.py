@@ -179,7 +179,7 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
         assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
 
 
-K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4)]
+K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
 
 
 @pytest.mark.parametrize("shape", [(2000, 200, 2000), (1500, 100, 3000), (2100, 56, 1030)])

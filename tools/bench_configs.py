@@ -151,7 +151,7 @@ def main():
         sampler.samples = []
         if not a.skip_blocks:
             blocks = []
-            for (bm, bn, st) in [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4)]:
+            for (bm, bn, st) in [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]:
                 q = moa.Plan(**{**pl.__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
                 rb = rec(N, N, N, timed(lambda: moa.gemm_with_plan(A, B, C, q), min(a.window, 0.5), sampler, est),
                          FP64_DMMA_PEAK_TFLOPS)
