@@ -20,6 +20,8 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257]
+# every compiled K1 tile config (bm, bn, stages), incl. the latency tiles
+K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
 
 
 def _moa():
@@ -171,15 +173,12 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
     tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
     base = moa.plan(m, n, p)
     assert base.kernel == "dgemm_tma"
-    for (bm, bn, st) in [(128, 128, 6), (128, 64, 4), (64, 64, 4)]:
-        pl = moa.Plan(**{**base.__dict__, "bm": bm, "bn": bn, "stages": st})
+    for (bm, bn, st) in K1_CONFIGS:
+        pl = moa.Plan(**{**base.__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
         out = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
         moa.gemm_with_plan(tA, tB, out, pl)
         torch.cuda.synchronize()
         assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
-
-
-K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
 
 
 @pytest.mark.parametrize("shape", [(2000, 200, 2000), (1500, 100, 3000), (2100, 56, 1030)])
