@@ -476,6 +476,7 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
+    RelaxedCapture relaxed_capture;
     attr_err = k1_attrs<BM, BN, WM, WN, ST, false>();
     if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true>();
   });
@@ -540,6 +541,7 @@ int k1_occupancy() {
 void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
+    RelaxedCapture relaxed_capture;
     int o[6] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
                 k1_occupancy<64, 32, 2, 2, 4>(), k1_occupancy<16, 32, 1, 2, 4>(), k1_occupancy<16, 16, 1, 1, 4>()};
     for (int i = 0; i < 6; ++i)

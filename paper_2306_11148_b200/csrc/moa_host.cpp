@@ -76,6 +76,7 @@ int get_device_shape(int device, DeviceShape* out) {
   d.device = device;
   cudaError_t e;
   int v = 0;
+  RelaxedCapture relaxed_capture;  // first call may be inside graph capture
   if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
     return cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
   cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, device);

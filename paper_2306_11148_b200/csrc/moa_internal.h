@@ -10,6 +10,19 @@
 
 namespace moa {
 
+// One-time library setup (pool allocation, kernel attributes, occupancy queries)
+// may run during the caller's first call, which may be inside CUDA-graph stream
+// capture. Those calls are not stream work, so the thread switches to relaxed
+// capture mode for their duration (restored on scope exit).
+struct RelaxedCapture {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+  RelaxedCapture(const RelaxedCapture&) = delete;
+  RelaxedCapture& operator=(const RelaxedCapture&) = delete;
+};
+
+
 // Per-device properties the static plan reads (cached, mutex-guarded).
 struct DeviceShape {
   int device = -1;

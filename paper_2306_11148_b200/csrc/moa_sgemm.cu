@@ -293,6 +293,7 @@ TileConfig kK3gConfigs[] = {
 void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
+    RelaxedCapture relaxed_capture;
     int n = 0;
     auto kern = k_sgemm_ffma<6, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K3Traits<6>::kSmem) == cudaSuccess &&
@@ -333,6 +334,7 @@ int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t st
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
+    RelaxedCapture relaxed_capture;
     attr_err = cudaFuncSetAttribute(k_sgemm_ffma<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(k_sgemm_ffma<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);

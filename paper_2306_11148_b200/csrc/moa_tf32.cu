@@ -539,6 +539,7 @@ int launch_k4ts(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) 
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
+    RelaxedCapture relaxed_capture;
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
   });
   if (attr_err != cudaSuccess) {
@@ -580,6 +581,7 @@ int launch_k4(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
+    RelaxedCapture relaxed_capture;
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
   });
   if (attr_err != cudaSuccess) {

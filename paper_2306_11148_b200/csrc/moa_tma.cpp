@@ -14,6 +14,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
+    RelaxedCapture relaxed_capture;
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
@@ -62,7 +63,10 @@ bool acquire_tile_counter(cudaStream_t stream, unsigned int** out) {
   if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(g_ctr_mu);
     CounterPool& pool = g_ctr[device];
-    if (!pool.dev) e = cudaMalloc(&pool.dev, kCounterSlots * sizeof(unsigned int));  // library-owned, once
+    if (!pool.dev) {  // library-owned, once (capture-safe: not stream work)
+      RelaxedCapture relaxed_capture;
+      e = cudaMalloc(&pool.dev, kCounterSlots * sizeof(unsigned int));
+    }
     if (e == cudaSuccess) slot = pool.dev + (pool.next++ % kCounterSlots);
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(slot, 0, sizeof(unsigned int), stream);
@@ -100,9 +104,14 @@ bool acquire_split_flags(unsigned int count, unsigned int** out) {
   if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(g_flag_mu);
     FlagPool& pool = g_flag[device];
-    if (!pool.dev) {  // library-owned, once (not inside stream capture: the first GEMM call creates it)
+    if (!pool.dev) {  // library-owned, once; capture-safe: zeroed on a private stream
+      RelaxedCapture relaxed_capture;
+      cudaStream_t ps = nullptr;
       e = cudaMalloc(&pool.dev, kFlagSlots * sizeof(unsigned int));
-      if (e == cudaSuccess) e = cudaMemset(pool.dev, 0, kFlagSlots * sizeof(unsigned int));
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaMemsetAsync(pool.dev, 0, kFlagSlots * sizeof(unsigned int), ps);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ps);
+      if (ps) cudaStreamDestroy(ps);
     }
     if (e == cudaSuccess) {
       if (pool.next + count > kFlagSlots) pool.next = 0;
