@@ -288,6 +288,12 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (int)((n + kBK - 1) / kBK);
 
+  // Programmatic dependent launch: this prologue may run while the previous grid in
+  // the stream drains; griddepcontrol.wait (below) orders every global-memory access
+  // after that grid's completion, so stream semantics are unchanged. Each thread
+  // signals launch_dependents only when it is done, so the next grid's CTAs are
+  // placed as this grid's SMs free up (signalling at the start let small CTAs of the
+  // next grids pile onto busy SMs: N=512 went from 15 to 23 us).
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -297,6 +303,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     fence_mbar_init();
   }
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp >= Tr::kConsumerWarps) {
     // ----------------------------- producer ---------------------------------
@@ -364,6 +371,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
       desc[stage].t = -1;
       mbar_arrive(full0 + 8 * stage);
     }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
 
@@ -397,6 +405,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ------------------------------ K2: generic ----------------------------------
@@ -493,9 +502,19 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     // no counter when every tile is a stream-K run (tiles < 2G: run = CTA index)
     if (!(sk && sk_first_tile(plan.tiles, plan.grid) == 0) && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   }
-  kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                                       plan.raster_group, flags, ctr);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)plan.grid);
+  cfg.blockDim = dim3(Tr::kThreads);
+  cfg.dynamicSmemBytes = Tr::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see the kernel prologue)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
+                                     (int)plan.raster_group, flags, ctr);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
     return MOA_ERR_CUDA;
