@@ -238,9 +238,7 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
     // alone does not do it (ptxas even hoists the arrive above the slab's last
     // DMMAs): without this fence whole warp tiles were computed from overwritten
     // operands, rarely under dynamic scheduling, often under stream-K.
-#ifndef MOA_AB_NO_PROXY_FENCE  // A/B cost measurement only (tools/build_variant.sh); never set in the product
     fence_proxy_async_smem();
-#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * stage);
     if (++stage == STAGES) {
