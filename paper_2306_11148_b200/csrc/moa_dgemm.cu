@@ -2,11 +2,15 @@
 //
 //   C[(i*p)+j] := sum_k A[(i*n)+k] * B[(k*p)+j]      (Eq. 3)
 //
-// K1 k_dgemm_tma   : persistent, warp-specialised. One producer warp streams the
-//                    operands with TMA (cp.async.bulk.tensor, 128B swizzle) into
-//                    an S-stage shared-memory ring guarded by mbarriers; 2..8
-//                    consumer warps run DMMA.8x8x4 (mma.sync m8n8k4 f64) on
-//                    register accumulators.
+// K1 k_dgemm_tma   : persistent, warp-specialised. A producer warp (a warpgroup
+//                    that donates its registers, for the 128x128 tile) streams
+//                    the operands with TMA (cp.async.bulk.tensor, 128B swizzle)
+//                    into an S-stage shared-memory ring guarded by mbarriers;
+//                    1..8 consumer warps run DMMA.8x8x4 (mma.sync m8n8k4 f64) on
+//                    register accumulators. Work: dynamically claimed tiles plus
+//                    stream-K runs for the partial last wave, whose cut tiles
+//                    continue the fma chain from the stored partial (bitwise);
+//                    launched with programmatic dependent launch.
 // K2 k_dgemm_generic: same arithmetic, plain predicated loads (odd n or p,
 //                    pointers not 16-byte aligned — shapes TMA cannot describe).
 //
