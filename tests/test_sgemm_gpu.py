@@ -118,6 +118,30 @@ def test_3xtf32_tolerance_and_truth_error(cuda_device):
         assert err_truth <= 1e-5 * np.sqrt(n), (m, n, p, err_truth)  # 3xTF32 ~ fp32-level accuracy
 
 
+def test_3xtf32_config2_n16384_sampled_rows(cuda_device):
+    """BASELINE configs[2] tensor-core variant at full size (fp32 N=16384, 3xTF32):
+    sampled rows within the north_star 5e-3 of the literal ip.c and within fp32-level
+    error of the fp64-accumulated truth; plus a Freivalds check of all of C."""
+    import torch
+    moa = _moa()
+    N = 16384
+    tA = torch.empty((N, N), dtype=torch.float32, device=cuda_device)
+    tB = torch.empty((N, N), dtype=torch.float32, device=cuda_device)
+    I.device_fill(tA, 1, I.ID_A)
+    I.device_fill(tB, 1, I.ID_B)
+    C = moa.gemm(tA, tB, precision="3xtf32")
+    torch.cuda.synchronize()
+    rows = [0, 127, 128, 8191, N - 1]
+    B = I.host_matrix(N, N, 1, I.ID_B, dtype=np.float32)
+    Ar = I.host_rows(rows, N, 1, I.ID_A, dtype=np.float32)
+    got = C[torch.tensor(rows, device=cuda_device)].cpu().numpy()
+    assert _relfro(got, O.ip_rowblock(Ar, B, fused=False)) <= 5e-3
+    assert _relfro(got, O.ip_f32_truth(Ar, B)) <= 1e-5 * np.sqrt(N)
+    x = torch.randint(0, 2, (N, 1), generator=torch.Generator().manual_seed(3)).to(tA) * 2 - 1
+    y, z = C.double() @ x.double(), tA.double() @ (tB.double() @ x.double())
+    assert float(torch.linalg.norm(y - z) / torch.linalg.norm(z)) <= 5e-3
+
+
 def test_3xtf32_integer_inputs_exact(cuda_device):
     """Values in {-4..4} are exact in TF32 (small part 0) and every partial sum is an
     integer < 2^24: the tensor-core result must equal the oracle bit for bit (P6)."""
