@@ -24,6 +24,7 @@
 #ifndef MOA_H
 #define MOA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -48,7 +49,8 @@ typedef enum {
   MOA_ERR_INVALID_INDEX = 6,   /* psi index out of bounds (0 <=* i <* rho xi) */
   MOA_ERR_CUDA = 7,
   MOA_ERR_NCCL = 8,
-  MOA_ERR_UNSUPPORTED_DEVICE = 9 /* not an sm_100 device */
+  MOA_ERR_UNSUPPORTED_DEVICE = 9, /* not an sm_100 device */
+  MOA_ERR_NOT_REGISTERED = 10     /* pointer is not inside a window of the communicator */
 } moa_status;
 
 /* Kernels the static plan can choose. */
@@ -194,6 +196,52 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
  * use of a grid shape and cached in the communicator. Bitwise equal to one GPU. */
 int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
                        void* C_block, int dtype, void* stream, moa_comm_t comm);
+
+/* ------------------------------------------------------------------------
+ * The row-lifted GEMM with the all-gather of C FUSED into the GEMM (SURVEY §8(f)
+ * NEXT-1 step 3; reading R14: every rank ends with all of C). Instead of a GEMM
+ * followed by ncclAllGather, the epilogue of the GEMM kernel stores every final C
+ * tile of rank g's rows [row0_g, row0_g + rows_g) both into its own C_full and,
+ * over NVLink, into every other rank's C_full at the same rows — so the exchange
+ * of C overlaps the remaining tiles' tensor-core work instead of following it.
+ *
+ * moa_gemm_scatter — the epilogue on its own (usable on one GPU): moa_gemm_acc
+ * (same arguments, same result in C), and every final C tile is also written to
+ * dst[0..ndst): each an m x p row-major block with row stride ldc (DEVICE address;
+ * may be a peer GPU's memory mapped into this process, e.g. from
+ * moa_comm_window_peer). Every destination receives exactly the bits of C. With
+ * accumulate != 0 (the last k-panel of a chain) only C is read. MOA_F64 only
+ * (MOA_ERR_INVALID_DTYPE); 0 <= ndst <= 8 (MOA_ERR_INVALID_SHAPE); destinations
+ * non-NULL when m*p > 0, aligned to 8 bytes, and disjoint from A, B, C and each
+ * other (MOA_ERR_ALIASING). Asynchronous on `stream`. */
+int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                     void* C, int64_t ldc, int accumulate, int ndst, void* const* dst, int dtype, void* stream);
+
+/* moa_comm_alloc_window — COLLECTIVE (every rank, same bytes): allocate `bytes` of
+ * device memory on each rank with ncclMemAlloc and register it on the
+ * communicator as an NCCL symmetric window (NCCL_WIN_COLL_SYMMETRIC), so every
+ * rank's copy is load/store-reachable from every GPU; *ptr = this rank's copy.
+ * The library owns the memory until moa_comm_free_window (COLLECTIVE) or
+ * moa_comm_destroy. MOA_ERR_NCCL if not every rank is in the NVLink
+ * load/store domain (NCCL's LSA team) or registration fails.
+ * moa_comm_window_peer — *out = this process's address of rank `peer`'s copy of
+ * the window byte that `ptr` addresses in this rank's copy (for peer == rank, an
+ * alias of ptr's memory at another virtual address; MOA_ERR_NOT_REGISTERED
+ * if ptr is not inside a window; MOA_ERR_INVALID_INDEX for a bad peer). */
+int moa_comm_alloc_window(moa_comm_t comm, size_t bytes, void** ptr);
+int moa_comm_free_window(moa_comm_t comm, void* ptr);
+int moa_comm_window_peer(moa_comm_t comm, const void* ptr, int peer, void** out);
+
+/* moa_gemm_lifted_gather — row-lifted C := A • B with the fused gather. COLLECTIVE.
+ *   A_local, B, m, n, p, npanels: as moa_gemm_lifted_ex (B broadcast from rank 0).
+ *   C_full : m x p, inside a window from moa_comm_alloc_window on every rank
+ *            (MOA_ERR_NOT_REGISTERED otherwise). On return (stream order) every
+ *            rank's C_full holds all of C, bitwise equal to moa_gemm on one GPU.
+ * Stream order: a one-element all-reduce barrier before the GEMM (no rank stores
+ * into a peer's C_full before that peer reached this call) and one after it (all
+ * peer stores are complete). MOA_F64 only; at most 9 ranks (one NVLink node). */
+int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_full, int dtype,
+                           void* stream, moa_comm_t comm, int npanels);
 
 /* moa_lift_panels — static k-panel count for the lifted exchange: 1 when B does
  * not travel (nranks == 1), else ceil(bytes(B) / 512 MiB) clamped to [1, 8] and

@@ -22,7 +22,8 @@ from typing import Optional, Sequence
 __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
-    "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols", "gemm_lifted_2d",
+    "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols", "gemm_lifted_2d", "gemm_scatter",
+    "gemm_lifted_gather",
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
@@ -65,6 +66,12 @@ _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _v
 _moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
 _moa_gemm_lifted_cols = _sig("moa_gemm_lifted_cols", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_lifted_2d = _sig("moa_gemm_lifted_2d", [_i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp])
+_moa_gemm_scatter = _sig("moa_gemm_scatter", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32,
+                                              ctypes.POINTER(_vp), _i32, _vp])
+_moa_gemm_lifted_gather = _sig("moa_gemm_lifted_gather", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
+_moa_comm_alloc_window = _sig("moa_comm_alloc_window", [_vp, ctypes.c_size_t, ctypes.POINTER(_vp)])
+_moa_comm_free_window = _sig("moa_comm_free_window", [_vp, _vp])
+_moa_comm_window_peer = _sig("moa_comm_window_peer", [_vp, _vp, _i32, ctypes.POINTER(_vp)])
 _moa_hadamard = _sig("moa_hadamard", [_i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_kron = _sig("moa_kron", [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_psi = _sig("moa_psi", [_i32, ctypes.POINTER(_i64), _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
@@ -349,8 +356,44 @@ class Comm:
     def handle(self):
         return self._h
 
+    def alloc_window(self, shape: Sequence[int], dtype=None):
+        """COLLECTIVE: a tensor of `shape` in NCCL symmetric memory registered on this
+        communicator (moa_comm_alloc_window) — the C_full of gemm_lifted_gather. The
+        library owns the memory; release it with free_window (collective) or close()."""
+        torch = _torch()
+        dtype = torch.float64 if dtype is None else dtype
+        numel = 1
+        for d in shape:
+            numel *= int(d)
+        esize = torch.empty((), dtype=dtype).element_size()
+        ptr = _vp()
+        _check(_moa_comm_alloc_window(self._h, max(1, numel) * esize, ctypes.byref(ptr)), "moa_comm_alloc_window")
+        typestr = {torch.float64: "<f8", torch.float32: "<f4"}[dtype]
+
+        class _Mem:  # __cuda_array_interface__ view of the library-owned window
+            __cuda_array_interface__ = {"shape": tuple(int(d) for d in shape), "typestr": typestr,
+                                        "data": (int(ptr.value), False), "version": 3, "strides": None,
+                                        "stream": None}
+        t = torch.as_tensor(_Mem(), device=torch.device("cuda", self.device))
+        self._windows = getattr(self, "_windows", {})
+        self._windows[int(ptr.value)] = t
+        return t
+
+    def free_window(self, t) -> None:
+        """COLLECTIVE: release a tensor from alloc_window (moa_comm_free_window)."""
+        ptr = t.data_ptr()
+        getattr(self, "_windows", {}).pop(ptr, None)
+        _check(_moa_comm_free_window(self._h, ptr), "moa_comm_free_window")
+
+    def window_peer(self, t, peer: int) -> int:
+        """Address, in this process, of rank `peer`'s copy of window tensor t's first element."""
+        out = _vp()
+        _check(_moa_comm_window_peer(self._h, t.data_ptr(), peer, ctypes.byref(out)), "moa_comm_window_peer")
+        return int(out.value or 0)
+
     def close(self):
         if self._h:
+            getattr(self, "_windows", {}).clear()
             _check(_moa_comm_destroy(self._h), "moa_comm_destroy")
             self._h = None
 
@@ -376,6 +419,42 @@ def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precisi
                                C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
                                code, _stream_ptr(stream), comm.handle, npanels), "moa_gemm_lifted_ex")
     return C_local
+
+
+def gemm_lifted_gather(m: int, A_local, B, C_full, comm: Comm, *, stream=None, npanels: int = 0):
+    """Row-lifted C := A • B with the all-gather of C fused into the GEMM epilogue
+    (moa_gemm_lifted_gather; collective). C_full (m x p fp64) must come from
+    comm.alloc_window; on return (stream order) it holds all of C on every rank."""
+    n, p = B.shape
+    for name, t in (("A_local", A_local), ("B", B), ("C_full", C_full)):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    _check(_moa_gemm_lifted_gather(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None,
+                                   C_full.data_ptr() or None, _dtype_code(B), _stream_ptr(stream), comm.handle,
+                                   npanels), "moa_gemm_lifted_gather")
+    return C_full
+
+
+def gemm_scatter(A, B, out, dsts, *, accumulate: bool = False, stream=None):
+    """C (+)= A • B (fp64; moa_gemm_acc semantics) whose epilogue also writes every
+    final C tile to each tensor (or raw device address) in `dsts` — the fused-gather
+    epilogue on one GPU (moa_gemm_scatter). A and B may be row-strided 2-D views
+    (e.g. a k-panel A[:, k0:k1], B[k0:k1, :]); out and every dst are m x p contiguous."""
+    m, n = A.shape
+    p = B.shape[1]
+    if B.shape[0] != n or tuple(out.shape) != (m, p):
+        raise ValueError("shape mismatch")
+    for name, t in (("A", A), ("B", B)):
+        if not t.is_cuda or t.stride(1) != 1:
+            raise ValueError(f"{name} must be a row-major CUDA view")
+    if not out.is_cuda or not out.is_contiguous():
+        raise ValueError("out must be a contiguous CUDA tensor")
+    addrs = [d if isinstance(d, int) else d.data_ptr() for d in dsts]
+    arr = (_vp * max(1, len(addrs)))(*[a or None for a in addrs])
+    _check(_moa_gemm_scatter(m, n, p, A.data_ptr() or None, max(1, A.stride(0)), B.data_ptr() or None,
+                             max(1, B.stride(0)), out.data_ptr() or None, max(1, p), 1 if accumulate else 0,
+                             len(addrs), arr, _dtype_code(A), _stream_ptr(stream)), "moa_gemm_scatter")
+    return out
 
 
 def gemm_lifted_cols(A, B_local, C_local, p: int, comm: Comm, C_full=None, workspace=None, *, stream=None):

@@ -272,13 +272,19 @@ struct PieceDesc {
   int32_t k0, k1, run, pad;
 };
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC>
+//
+// PEER: the fused GEMM -> all-gather epilogue (moa_gemm_lifted_gather). Every FINAL
+// tile (whole tile, or the tail of a stream-K cut tile) is also stored, straight
+// from the accumulator registers, to each peers.dst[d] at the same (row, col) —
+// NVLink peer stores into the other ranks' C_full, overlapping the remaining
+// tiles' DMMA work; stream-K head partials stay local.
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC, bool PEER>
 __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads,
                                   K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ flags,
-                unsigned int* __restrict__ tile_ctr) {
+                unsigned int* __restrict__ tile_ctr, const __grid_constant__ PeerDst peers) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -406,6 +412,12 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
                                                                    ACC || tail, f, lane);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
+    if constexpr (PEER) {
+      if (!head)
+        for (int d = 0; d < peers.nd; ++d)
+          store_acc<Tr::kMA, Tr::kNBox, true>(acc, reinterpret_cast<double*>(peers.dst[d]), m, p, ldc,
+                                              tm * BM + wm * 8 * Tr::kMA, tn * BN + wn * Tr::kNBox * 16, f);
+    }
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -415,7 +427,7 @@ template <int BM, int BN, int WARPS_M, int WARPS_N>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     k_dgemm_generic(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int64_t m,
                     int64_t n, int64_t p, int64_t lda, int64_t ldb, int64_t ldc, int accumulate, int64_t tiles_m,
-                    int64_t tiles_n, int group) {
+                    int64_t tiles_n, int group, const __grid_constant__ PeerDst peers) {
   constexpr int kNBox = BN / WARPS_N / 16;
   constexpr int kThreads = WARPS_M * WARPS_N * 32;
   __shared__ __align__(1024) uint8_t sm[(BM + BN) * kRowBytes];
@@ -455,6 +467,9 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
       mma_slab(acc, sa + wm * 32 * kRowBytes, sb + wn * kNBox * kBoxBytes, f);
     }
     store_acc<4, kNBox, false>(acc, C, m, p, ldc, row0 + wm * 32, col0 + wn * kNBox * 16, f);
+    for (int d = 0; d < peers.nd; ++d)  // fused gather epilogue (see K1's PEER)
+      store_acc<4, kNBox, false>(acc, reinterpret_cast<double*>(peers.dst[d]), m, p, ldc, row0 + wm * 32,
+                                 col0 + wn * kNBox * 16, f);
   }
 }
 
@@ -467,9 +482,9 @@ bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 // Opt in to the full dynamic smem per CTA and the maximum shared-memory carveout:
 // without the carveout the driver picked a smaller L1/smem split and the small
 // tiles fit fewer CTAs per SM than their smem allows (32x32x3: 6 instead of 8).
-template <int BM, int BN, int WM, int WN, int ST, bool ACC>
+template <int BM, int BN, int WM, int WN, int ST, bool ACC, bool PEER>
 cudaError_t k1_attrs() {
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC, PEER>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        K1Traits<BM, BN, WM, WN, ST>::kSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -483,13 +498,20 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   const int64_t m = g.m, n = g.n, p = g.p;
   if (!encode_2d_f64(&ta, g.A, m, n, g.lda, BM) || !encode_2d_f64(&tb, g.B, n, p, g.ldb, 16)) return MOA_ERR_CUDA;
   double* C = (double*)g.C;
-  auto kern = g.accumulate ? k_dgemm_tma<BM, BN, WM, WN, ST, true> : k_dgemm_tma<BM, BN, WM, WN, ST, false>;
+  const bool peer = g.peers && g.peers->nd > 0;
+  auto kern = g.accumulate
+                  ? (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, true, true> : k_dgemm_tma<BM, BN, WM, WN, ST, true, false>)
+                  : (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, false, true> : k_dgemm_tma<BM, BN, WM, WN, ST, false, false>);
+  PeerDst peers{};
+  if (peer) peers = *g.peers;
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     RelaxedCapture relaxed_capture;
-    attr_err = k1_attrs<BM, BN, WM, WN, ST, false>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true>();
+    attr_err = k1_attrs<BM, BN, WM, WN, ST, false, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, false, true>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, true>();
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
@@ -515,7 +537,7 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                     (int)plan.raster_group, flags, ctr);
+                                     (int)plan.raster_group, flags, ctr, peers);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -552,8 +574,8 @@ TileConfig kK2Configs[] = {
 template <int BM, int BN, int WM, int WN, int ST>
 int k1_occupancy() {
   using Tr = K1Traits<BM, BN, WM, WN, ST>;
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false>;
-  if (k1_attrs<BM, BN, WM, WN, ST, false>() != cudaSuccess) return 0;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false, false>;
+  if (k1_attrs<BM, BN, WM, WN, ST, false, false>() != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Tr::kThreads, Tr::kSmem) != cudaSuccess) return 0;
   return n;
@@ -602,9 +624,11 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
 }
 
 int launch_dgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  PeerDst peers{};
+  if (g.peers) peers = *g.peers;
   k_dgemm_generic<64, 64, 2, 2><<<plan.grid, 128, 0, stream>>>(
       (const double*)g.A, (const double*)g.B, (double*)g.C, g.m, g.n, g.p, g.lda, g.ldb, g.ldc, g.accumulate,
-      plan.tiles_m, plan.tiles_n, plan.raster_group);
+      plan.tiles_m, plan.tiles_n, plan.raster_group, peers);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_generic launch: ") + cudaGetErrorString(e));

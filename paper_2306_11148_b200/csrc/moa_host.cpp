@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "moa.h"
 #include "moa_internal.h"
@@ -31,6 +32,17 @@ struct moa_comm_s {
   // 2-D lifting: row / column sub-communicators for the last grid shape used
   int grid_rows = 0, grid_cols = 0;
   ncclComm_t row_comm = nullptr, col_comm = nullptr;
+  // Symmetric windows (moa_comm_alloc_window) for the fused GEMM -> all-gather:
+  // ncclMemAlloc'd memory registered on this communicator, with every rank's copy
+  // resolved to an address in this process.
+  struct Window {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ncclWindow_t win = nullptr;
+    std::vector<void*> peer;  // peer[r] = rank r's copy
+  };
+  std::vector<Window> windows;
+  int* barrier_buf = nullptr;  // one int, the operand of the barrier all-reduce
 };
 
 namespace moa {
@@ -310,6 +322,8 @@ int run_plan(const moa_plan_t& plan, const GemmArgs& g, int dtype, cudaStream_t 
       if (g.accumulate) return MOA_OK;
       const size_t es = (size_t)elem_size(dtype);
       cudaError_t e = cudaMemset2DAsync(g.C, (size_t)g.ldc * es, 0, (size_t)g.p * es, (size_t)g.m, s);
+      for (int d = 0; g.peers && d < g.peers->nd && e == cudaSuccess; ++d)
+        e = cudaMemset2DAsync(g.peers->dst[d], (size_t)g.ldc * es, 0, (size_t)g.p * es, (size_t)g.m, s);
       return e == cudaSuccess ? MOA_OK : cuda_fail(e, "cudaMemset2DAsync");
     }
     case MOA_KERNEL_DGEMM_TMA: return launch_dgemm_tma(plan, g, s);
@@ -326,6 +340,10 @@ int run_plan(const moa_plan_t& plan, const GemmArgs& g, int dtype, cudaStream_t 
 int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t stream) {
   int rc = validate_g(g, dtype);
   if (rc) return rc;
+  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64) {
+    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 only");
+    return MOA_ERR_INVALID_DTYPE;
+  }
   DeviceShape ds;
   if ((rc = get_device_shape(-1, &ds))) return rc;
   if ((rc = check_device(ds))) return rc;
@@ -398,6 +416,7 @@ const char* moa_status_string(int status) {
     case MOA_ERR_CUDA: return "MOA_ERR_CUDA";
     case MOA_ERR_NCCL: return "MOA_ERR_NCCL";
     case MOA_ERR_UNSUPPORTED_DEVICE: return "MOA_ERR_UNSUPPORTED_DEVICE";
+    case MOA_ERR_NOT_REGISTERED: return "MOA_ERR_NOT_REGISTERED";
     default: return "MOA_ERR_UNKNOWN";
   }
 }
@@ -674,6 +693,13 @@ int moa_comm_destroy(moa_comm_t comm) {
   if (comm->row_comm) ncclCommDestroy(comm->row_comm);
   if (comm->col_comm) ncclCommDestroy(comm->col_comm);
   if (comm->side) cudaStreamSynchronize(comm->side);
+  for (auto& w : comm->windows) {
+    cudaDeviceSynchronize();  // no kernel may still be storing into the window
+    ncclCommWindowDeregister(comm->nccl, w.win);
+    ncclMemFree(w.ptr);
+  }
+  comm->windows.clear();
+  if (comm->barrier_buf) cudaFree(comm->barrier_buf);
   for (int i = 0; i < kMaxPanels; ++i)
     if (comm->ev_panel[i]) cudaEventDestroy(comm->ev_panel[i]);
   if (comm->ev_start) cudaEventDestroy(comm->ev_start);
@@ -754,42 +780,16 @@ int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks) {
   return k < 1 ? 1 : (int)k;
 }
 
-int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
-                       int dtype, void* stream, moa_comm_t comm, int npanels) {
-  if (!comm) {
-    set_error("NULL communicator");
-    return MOA_ERR_NULL_POINTER;
-  }
-  if (m < 0) {
-    set_error("negative extent");
-    return MOA_ERR_INVALID_SHAPE;
-  }
-  if (npanels < 0 || npanels > kMaxPanels) {
-    set_error("npanels out of range");
-    return MOA_ERR_INVALID_SHAPE;
-  }
-  int64_t row0 = 0, rows = 0;
-  int rc = moa_lift_rows(m, comm->nranks, comm->rank, &row0, &rows);
-  if (rc) return rc;
-  if ((rc = validate(rows, n, p, A_local, B, C_local, dtype))) return rc;
+// Steps (1)-(2) of the row-lifted GEMM, shared by moa_gemm_lifted_ex and
+// moa_gemm_lifted_gather: the broadcast of B (optionally pipelined in k-panels) and
+// this rank's rows of C. `last_peers` (fused gather) goes to the launch that writes
+// the FINAL C, i.e. the last k-panel.
+static int lifted_bcast_compute(int64_t n, int64_t p, int64_t rows, const void* A_local, void* B, void* C_local,
+                                int dtype, cudaStream_t s, moa_comm_t comm, int npanels, const PeerDst* last_peers) {
   const int64_t es = elem_size(dtype);
-  if (C_full && (reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
-    set_error("C_full not aligned to the element size");
-    return MOA_ERR_MISALIGNED;
-  }
-  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
-    if (!x || !y || xb <= 0 || yb <= 0) return false;
-    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
-    return a0 < b1 && b0 < a1;
-  };
-  if (C_full && (overlap(C_full, m * p * es, B, n * p * es) || overlap(C_full, m * p * es, A_local, rows * n * es) ||
-                 overlap(C_full, m * p * es, C_local, rows * p * es))) {
-    set_error("C_full overlaps another operand");
-    return MOA_ERR_ALIASING;
-  }
-  cudaStream_t s = (cudaStream_t)stream;
   const ncclDataType_t ty = nccl_type(dtype);
   cudaError_t e;
+  int rc;
   int K = npanels > 0 ? npanels : moa_lift_panels(n, p, dtype, comm->nranks);
   if (n < K) K = n > 0 ? (int)n : 1;
   // k-panel boundaries: multiples of 32 rows of B (TMA alignment of the A column
@@ -833,8 +833,49 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
     if (k1 <= k0 && j > 0) continue;
     GemmArgs g{rows, k1 - k0, p, (const char*)A_local + k0 * es, (const char*)B + k0 * p * es, C_local,
                n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
+    if (j == K - 1) g.peers = last_peers;  // the final panel writes the final C
     if ((rc = gemm_impl(g, dtype, nullptr, s))) return rc;
   }
+  return MOA_OK;
+}
+
+int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
+                       int dtype, void* stream, moa_comm_t comm, int npanels) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (m < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if (npanels < 0 || npanels > kMaxPanels) {
+    set_error("npanels out of range");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t row0 = 0, rows = 0;
+  int rc = moa_lift_rows(m, comm->nranks, comm->rank, &row0, &rows);
+  if (rc) return rc;
+  if ((rc = validate(rows, n, p, A_local, B, C_local, dtype))) return rc;
+  const int64_t es = elem_size(dtype);
+  if (C_full && (reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
+    set_error("C_full not aligned to the element size");
+    return MOA_ERR_MISALIGNED;
+  }
+  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
+    if (!x || !y || xb <= 0 || yb <= 0) return false;
+    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
+    return a0 < b1 && b0 < a1;
+  };
+  if (C_full && (overlap(C_full, m * p * es, B, n * p * es) || overlap(C_full, m * p * es, A_local, rows * n * es) ||
+                 overlap(C_full, m * p * es, C_local, rows * p * es))) {
+    set_error("C_full overlaps another operand");
+    return MOA_ERR_ALIASING;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = lifted_bcast_compute(n, p, rows, A_local, B, C_local, dtype, s, comm, npanels, nullptr))) return rc;
+  const ncclDataType_t ty = nccl_type(dtype);
+  cudaError_t e;
   // (3) optional gather of C (reading R14).
   if (C_full && m * p > 0) {
     if (comm->nranks == 1) {
@@ -964,3 +1005,224 @@ int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* 
 }
 
 }  // extern "C"
+
+// ----------------------- fused GEMM -> all-gather (NEXT-1) -----------------------
+
+int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                     void* C, int64_t ldc, int accumulate, int ndst, void* const* dst, int dtype, void* stream) {
+  if (ndst < 0 || ndst > kMaxPeerDst) {
+    set_error("ndst out of range [0, 8]");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  GemmArgs g{m, n, p, A, B, C, lda, ldb, ldc, accumulate ? 1 : 0};
+  int rc = validate_g(g, dtype);
+  if (rc) return rc;
+  if (ndst > 0 && dtype != MOA_F64) {
+    set_error("moa_gemm_scatter: MOA_F64 only");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  const int64_t es = elem_size(dtype);
+  if (ndst > 0 && m * p > 0 && !dst) {
+    set_error("NULL dst array");
+    return MOA_ERR_NULL_POINTER;
+  }
+  PeerDst pd{};
+  pd.nd = m * p > 0 ? ndst : 0;
+  const int64_t cb = m * p > 0 ? ((m - 1) * ldc + p) * es : 0;  // byte span of one strided m x p block
+  auto ov = [cb](const void* x, const void* y, int64_t yb) {
+    if (!x || !y || cb <= 0 || yb <= 0) return false;
+    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)cb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
+    return a0 < b1 && b0 < a1;
+  };
+  for (int d = 0; d < pd.nd; ++d) {
+    void* q = dst[d];
+    if (!q) {
+      set_error("NULL destination");
+      return MOA_ERR_NULL_POINTER;
+    }
+    if (reinterpret_cast<uintptr_t>(q) % (uintptr_t)es) {
+      set_error("destination not aligned to the element size");
+      return MOA_ERR_MISALIGNED;
+    }
+    const int64_t ab = m * n > 0 ? ((m - 1) * lda + n) * es : 0, bb = n * p > 0 ? ((n - 1) * ldb + p) * es : 0;
+    bool bad = ov(q, A, ab) || ov(q, B, bb) || ov(q, C, cb);
+    for (int e2 = 0; e2 < d && !bad; ++e2) bad = ov(q, dst[e2], cb);
+    if (bad) {
+      set_error("destination overlaps an operand or another destination");
+      return MOA_ERR_ALIASING;
+    }
+    pd.dst[d] = q;
+  }
+  g.peers = &pd;
+  return gemm_impl(g, dtype, nullptr, (cudaStream_t)stream);
+}
+
+int moa_comm_alloc_window(moa_comm_t comm, size_t bytes, void** ptr) {
+  if (!comm || !ptr) {
+    set_error("NULL communicator or output pointer");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (bytes == 0) {
+    set_error("zero-byte window");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  // every rank must be load/store-reachable (one NVLink/NVSwitch domain)
+  if (lsa_team_size(comm->nccl) != comm->nranks) {
+    set_error("not every rank is NVLink load/store-reachable (LSA team smaller than the communicator)");
+    return MOA_ERR_NCCL;
+  }
+  cudaError_t e = cudaSetDevice(comm->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  if (!comm->barrier_buf) {
+    RelaxedCapture relaxed_capture;
+    if ((e = cudaMalloc(&comm->barrier_buf, sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc(barrier)");
+    if ((e = cudaMemset(comm->barrier_buf, 0, sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMemset(barrier)");
+  }
+  const size_t sz = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+  moa_comm_s::Window w;
+  w.bytes = bytes;
+  ncclResult_t r = ncclMemAlloc(&w.ptr, sz);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclMemAlloc");
+  r = ncclCommWindowRegister(comm->nccl, w.ptr, sz, &w.win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    ncclMemFree(w.ptr);
+    return nccl_fail(r, "ncclCommWindowRegister");
+  }
+  w.peer.assign((size_t)comm->nranks, nullptr);
+  // (rank r's own entry is NCCL's flat LSA mapping of the same physical memory: a
+  // different virtual address than w.ptr)
+  int rc = resolve_window_peers((void*)w.win, comm->nranks, w.peer.data());
+  if (rc) {
+    ncclCommWindowDeregister(comm->nccl, w.win);
+    ncclMemFree(w.ptr);
+    return rc;
+  }
+  comm->windows.push_back(w);
+  *ptr = w.ptr;
+  return MOA_OK;
+}
+
+int moa_comm_free_window(moa_comm_t comm, void* ptr) {
+  if (!comm || !ptr) {
+    set_error("NULL communicator or pointer");
+    return MOA_ERR_NULL_POINTER;
+  }
+  for (size_t i = 0; i < comm->windows.size(); ++i)
+    if (comm->windows[i].ptr == ptr) {
+      cudaError_t e = cudaDeviceSynchronize();
+      ncclResult_t r = ncclCommWindowDeregister(comm->nccl, comm->windows[i].win);
+      ncclResult_t r2 = ncclMemFree(ptr);
+      comm->windows.erase(comm->windows.begin() + (long)i);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+      if (r != ncclSuccess) return nccl_fail(r, "ncclCommWindowDeregister");
+      if (r2 != ncclSuccess) return nccl_fail(r2, "ncclMemFree");
+      return MOA_OK;
+    }
+  set_error("pointer is not a window of this communicator");
+  return MOA_ERR_NOT_REGISTERED;
+}
+
+int moa_comm_window_peer(moa_comm_t comm, const void* ptr, int peer, void** out) {
+  if (!comm || !ptr || !out) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (peer < 0 || peer >= comm->nranks) {
+    set_error("peer out of range");
+    return MOA_ERR_INVALID_INDEX;
+  }
+  for (const auto& w : comm->windows) {
+    const uintptr_t a = (uintptr_t)ptr, b = (uintptr_t)w.ptr;
+    if (a >= b && a < b + w.bytes) {
+      *out = (char*)w.peer[(size_t)peer] + (a - b);
+      return MOA_OK;
+    }
+  }
+  set_error("pointer is not inside a window of this communicator");
+  return MOA_ERR_NOT_REGISTERED;
+}
+
+// Barrier of the fused gather: a one-element all-reduce on the stream. When it
+// completes on rank r, every rank has finished the work it enqueued before it (for
+// the exit barrier: its GEMM, whose peer stores are complete at kernel end).
+static int stream_barrier(moa_comm_t comm, cudaStream_t s) {
+  if (comm->nranks <= 1) return MOA_OK;
+  ncclResult_t r = ncclAllReduce(comm->barrier_buf, comm->barrier_buf, 1, ncclInt32, ncclMax, comm->nccl, s);
+  return r == ncclSuccess ? MOA_OK : nccl_fail(r, "ncclAllReduce(barrier)");
+}
+
+int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_full, int dtype,
+                           void* stream, moa_comm_t comm, int npanels) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (m < 0 || n < 0 || p < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if (npanels < 0 || npanels > kMaxPanels) {
+    set_error("npanels out of range");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if (dtype != MOA_F64) {
+    set_error("moa_gemm_lifted_gather: MOA_F64 only");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  if (comm->nranks - 1 > kMaxPeerDst) {
+    set_error("moa_gemm_lifted_gather: at most 9 ranks (one NVLink node)");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t row0 = 0, rows = 0;
+  int rc = moa_lift_rows(m, comm->nranks, comm->rank, &row0, &rows);
+  if (rc) return rc;
+  const int64_t es = elem_size(dtype);
+  int64_t mp;
+  if (!mul_ok(m, p, &mp) || !mul_ok(mp, es, &mp)) {
+    set_error("m*p overflows");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  // C_full must lie inside one of this communicator's symmetric windows
+  const moa_comm_s::Window* win = nullptr;
+  if (mp > 0) {
+    if (!C_full) {
+      set_error("NULL C_full");
+      return MOA_ERR_NULL_POINTER;
+    }
+    for (const auto& w : comm->windows) {
+      const uintptr_t a = (uintptr_t)C_full, b = (uintptr_t)w.ptr;
+      if (a >= b && a + (uintptr_t)mp <= b + w.bytes) win = &w;
+    }
+    if (!win) {
+      set_error("C_full is not inside a window from moa_comm_alloc_window (of m*p elements)");
+      return MOA_ERR_NOT_REGISTERED;
+    }
+  }
+  char* c_local = mp > 0 ? (char*)C_full + row0 * p * es : nullptr;
+  if ((rc = validate(rows, n, p, A_local, B, c_local, dtype))) return rc;
+  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
+    if (!x || !y || xb <= 0 || yb <= 0) return false;
+    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
+    return a0 < b1 && b0 < a1;
+  };
+  if (overlap(C_full, mp, B, n * p * es) || overlap(C_full, mp, A_local, rows * n * es)) {
+    set_error("C_full overlaps another operand");
+    return MOA_ERR_ALIASING;
+  }
+  if (mp == 0 && (n * p == 0 || comm->nranks == 1)) return MOA_OK;
+  // peers: every other rank's copy of C_full, at this rank's rows
+  PeerDst pd{};
+  if (win && rows > 0) {
+    const uintptr_t off = (uintptr_t)C_full - (uintptr_t)win->ptr + (uintptr_t)(row0 * p * es);
+    for (int r = 0; r < comm->nranks; ++r)
+      if (r != comm->rank) pd.dst[pd.nd++] = (char*)win->peer[(size_t)r] + off;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // entry barrier: no rank stores into a peer's C_full before that peer has reached
+  // this call in its stream order (its earlier readers of C_full are done)
+  if ((rc = stream_barrier(comm, s))) return rc;
+  if ((rc = lifted_bcast_compute(n, p, rows, A_local, B, c_local, dtype, s, comm, npanels, pd.nd ? &pd : nullptr)))
+    return rc;
+  // exit barrier: every rank's GEMM (and so its peer stores) has completed
+  return stream_barrier(comm, s);
+}

@@ -40,6 +40,16 @@ void set_error(const std::string& s);
 // One GEMM call as the kernels see it: row-major operands with leading dimensions
 // (elements) lda >= n, ldb >= p, ldc >= p; accumulate != 0 continues the chain
 // from the C in memory (C := C + A•B, each element's fma chain extended in k order).
+// Extra destinations of the FINAL C tile (the fused GEMM -> all-gather epilogue of
+// moa_gemm_lifted_gather): each dst[d] is an m x p row-major block with the same
+// leading dimension as C, typically a peer GPU's C_full rows reached over NVLink
+// (an NCCL symmetric-window address). Partial (stream-K head) values never go there.
+constexpr int kMaxPeerDst = 8;
+struct PeerDst {
+  int nd;
+  void* dst[kMaxPeerDst];
+};
+
 struct GemmArgs {
   int64_t m, n, p;
   const void* A;
@@ -47,6 +57,7 @@ struct GemmArgs {
   void* C;
   int64_t lda, ldb, ldc;
   int accumulate;
+  const PeerDst* peers = nullptr;  // fp64 only (K1/K2 epilogues); nullptr or nd == 0: none
 };
 
 // Kernel launchers (moa_dgemm.cu / moa_sgemm.cu / moa_tf32.cu). Arguments are
@@ -56,6 +67,12 @@ int launch_dgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t
 int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
 int launch_sgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
 int launch_sgemm_3xtf32(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream);
+
+// moa_window.cu: out[r] = this process's address of rank r's copy of an NCCL
+// symmetric window (ncclWindow_t passed as void*). Synchronous.
+int resolve_window_peers(void* win, int nranks, void** out);
+// Size of NCCL's load/store-accessible (NVLink) team of a communicator (ncclComm_t).
+int lsa_team_size(void* comm);
 
 // ipophp siblings (moa_ipophp.cu); dense row-major operands, validated by the host.
 int launch_hadamard(int64_t m, int64_t n, const void* A, const void* B, void* C, int dtype, cudaStream_t s);

@@ -1,0 +1,179 @@
+"""Row-lifted GEMM with the all-gather of C fused into the GEMM epilogue (SURVEY
+§8(f) NEXT-1 step 3; reading R14): moa_gemm_scatter (the epilogue on one GPU),
+the symmetric-window helpers and moa_gemm_lifted_gather.
+
+Rows of C depend only on the same rows of A and on all of B (Fig. 1), so the
+gathered C_full equals the one-GPU product; every destination of the epilogue must
+hold exactly the oracle's bits (fused ip.c, reading R3).
+
+CPU (`-m "not gpu"`): argument validation happens before any CUDA call.
+GPU: the scatter epilogue with up to 8 destinations on every schedule (latency
+tiles, 128x128 dynamic + stream-K with split tiles, the generic kernel, n = 0,
+accumulate chains), and the full collective path on a 1-rank NCCL communicator
+(window allocation, peer-address resolution, barriers, lifted compute).
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import paper_2306_11148_b200 as moa
+from inputs import inputs as I
+from oracle import oracle as O
+
+
+def test_scatter_validation_without_gpu():
+    A, B, C, D = 0x10000, 0x200000, 0x4000000, 0x8000000
+    arr = (moa._vp * 9)(*([D + i * 0x100000 for i in range(9)]))
+    f = moa._moa_gemm_scatter
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 9, arr, 0, None) == 1            # ndst > 8
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, -1, arr, 0, None) == 1           # ndst < 0
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, arr, 1, None) == 2            # fp32 + destinations
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, None, 0, None) == 3           # NULL dst array
+    bad = (moa._vp * 2)(D, None)
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 2, bad, 0, None) == 3            # NULL destination
+    mis = (moa._vp * 1)(D + 4)
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, mis, 0, None) == 5            # misaligned
+    for q in (C + 8, A + 16, B, D):
+        al = (moa._vp * 2)(D, q)
+        assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 2, al, 0, None) == 4         # overlaps C / A / B / dst[0]
+    assert f(4, 8, 8, A, 7, B, 8, C, 8, 0, 1, arr, 0, None) == 1            # lda < n (as moa_gemm_acc)
+    # the collective entry points: NULL communicator before anything else
+    assert moa._moa_gemm_lifted_gather(4, 4, 4, A, B, C, 0, None, None, 0) == 3
+    assert moa._moa_comm_alloc_window(None, 64, moa._vp()) == 3
+    assert moa._moa_status_string(10) == b"MOA_ERR_NOT_REGISTERED"
+
+
+# --------------------------------------------------------------------- GPU ----
+
+def _operands(m, n, p, seed, dev):
+    A = torch.empty((m, n), dtype=torch.float64, device=dev)
+    B = torch.empty((n, p), dtype=torch.float64, device=dev)
+    if m * n:
+        I.device_fill(A, seed, I.ID_A)
+    if n * p:
+        I.device_fill(B, seed, I.ID_B)
+    return A, B
+
+
+# (shape, what it exercises)
+_SHAPES = [
+    ((200, 144, 176), "latency tiles 16x32"),
+    ((2000, 48, 2000), "128x128 stream-K only (split tiles)"),
+    ((2600, 160, 2000), "128x128 dynamic tiles + stream-K runs"),
+    ((1000, 256, 300), "ragged tail"),
+    ((257, 33, 131), "generic kernel (odd n, p)"),
+    ((300, 0, 200), "n = 0: zero fill"),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,what", _SHAPES, ids=[w for _, w in _SHAPES])
+def test_scatter_every_destination_bitwise(cuda_device, shape, what):
+    m, n, p = shape
+    A, B = _operands(m, n, p, 7, cuda_device)
+    ref = O.ip(A.cpu().numpy(), B.cpu().numpy(), fused=True) if n else np.zeros((m, p))
+    for nd in (1, 3, 8):
+        C = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+        dst = [torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device) for _ in range(nd)]
+        moa.gemm_scatter(A, B, C, dst)
+        torch.cuda.synchronize()
+        assert np.array_equal(C.cpu().numpy(), ref), (what, nd)
+        for d, t in enumerate(dst):
+            assert torch.equal(t, C), (what, nd, d)
+    # ndst = 0 is plain moa_gemm (the non-PEER kernel)
+    C0 = moa.gemm_scatter(A, B, torch.empty((m, p), dtype=torch.float64, device=cuda_device), [])
+    torch.cuda.synchronize()
+    assert np.array_equal(C0.cpu().numpy(), ref)
+
+
+@pytest.mark.gpu
+def test_scatter_accumulate_chain_last_panel(cuda_device):
+    """The lifted path's pipelined k-panels: panel j > 0 continues every element's fma
+    chain from C; only the last panel (accumulate + destinations, K1 ACC+PEER) writes
+    the destinations, which must hold the one-launch bits."""
+    for (m, n, p) in [(1000, 1000, 300), (2000, 96, 2000), (129, 70, 131)]:
+        A, B = _operands(m, n, p, 8, cuda_device)
+        ref = moa.gemm(A, B)
+        C = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+        dst = [torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device) for _ in range(2)]
+        cuts = [0, (n // 3) // 32 * 32, (2 * n // 3) // 32 * 32, n]
+        for j in range(3):
+            k0, k1 = cuts[j], cuts[j + 1]
+            moa.gemm_scatter(A[:, k0:k1], B[k0:k1, :], C, dst if j == 2 else [], accumulate=j > 0)
+        torch.cuda.synchronize()
+        assert torch.equal(C, ref), (m, n, p)
+        for t in dst:
+            assert torch.equal(t, ref), (m, n, p)
+
+
+@pytest.mark.gpu
+def test_scatter_rejects_fp32(cuda_device):
+    A = torch.ones((64, 64), dtype=torch.float32, device=cuda_device)
+    C = torch.empty((64, 64), dtype=torch.float32, device=cuda_device)
+    d = torch.empty((64, 64), dtype=torch.float32, device=cuda_device)
+    with pytest.raises(moa.MoAError) as e:
+        moa.gemm_scatter(A, A, C, [d])
+    assert e.value.name == "MOA_ERR_INVALID_DTYPE"
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.gpu
+def test_lifted_gather_single_rank_nccl(cuda_device):
+    """The whole collective path on a 1-rank NCCL communicator: symmetric window
+    allocation and peer-address resolution (rank 0's own copy resolves to the local
+    pointer), entry/exit barriers, B broadcast (pipelined panels too) and the lifted
+    compute into C_full — bitwise moa_gemm."""
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        for (m, n, p) in [(1000, 256, 300), (2000, 48, 2000), (129, 64, 130)]:
+            A, B = _operands(m, n, p, 9, cuda_device)
+            ref = moa.gemm(A, B)
+            C_full = comm.alloc_window((m, p))
+            # rank 0's resolved address (NCCL's flat LSA mapping) aliases the same memory:
+            # the epilogue storing through it lands in C_full
+            peer0 = comm.window_peer(C_full, 0)
+            assert comm.window_peer(C_full[1:], 0) == peer0 + p * 8
+            C_full.fill_(float("nan"))
+            C_tmp = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+            moa.gemm_scatter(A, B, C_tmp, [peer0])
+            torch.cuda.synchronize()
+            assert torch.equal(C_full, ref) and torch.equal(C_tmp, ref)
+            for K in (0, 3):
+                C_full.fill_(float("nan"))
+                moa.gemm_lifted_gather(m, A, B, C_full, comm, npanels=K)
+                torch.cuda.synchronize()
+                assert torch.equal(C_full, ref), (m, n, p, K)
+            comm.free_window(C_full)
+        # C_full outside any window
+        A, B = _operands(64, 32, 64, 1, cuda_device)
+        plain = torch.empty((64, 64), dtype=torch.float64, device=cuda_device)
+        with pytest.raises(moa.MoAError) as e:
+            moa.gemm_lifted_gather(64, A, B, plain, comm)
+        assert e.value.name == "MOA_ERR_NOT_REGISTERED"
+        w = comm.alloc_window((64, 64), torch.float32)
+        with pytest.raises(moa.MoAError) as e:
+            moa.gemm_lifted_gather(64, A.float(), B.float(), w, comm)
+        assert e.value.name == "MOA_ERR_INVALID_DTYPE"
+        with pytest.raises(moa.MoAError) as e:
+            comm.window_peer(plain, 0)
+        assert e.value.name == "MOA_ERR_NOT_REGISTERED"
+    finally:
+        comm.close()
+        dist.destroy_process_group()
