@@ -10,6 +10,10 @@ paper's energy-vs-N sweep shape), through moa_gemm.
 N > 1: the row-lifted path (moa_gemm_lifted): rank g owns 8192 rows of A and C
 (weak scaling: m = 8192·N), n = p = 8192, B is broadcast from rank 0 over NVLink
 with NCCL every step (the path's one real exchange, reading R13).
+--gather nccl|fused adds the optional all-gather of C (reading R14): ncclAllGather
+after the GEMM, or fused into the GEMM epilogue (moa_gemm_lifted_gather: NVLink
+peer stores into NCCL symmetric windows). --lifted runs the lifted path at N = 1
+too (a 1-rank NCCL communicator), which exercises the N > 1 code on one GPU.
 
 Rank 0 prints ONE JSON line: value = GFLOP/s of the whole job (all ranks' flops
 ÷ the max-over-ranks device time of exactly K steps), plus roofline (DMMA fp64
@@ -41,14 +45,20 @@ METRIC = "fp64 GEMM GFLOP/s (joules/GEMM vs N in energy/sweep)"
 DATA = "synthetic (seeded splitmix64 uniform[-1,1), inputs/)"
 
 
-def workload_config(N, ws):
+def workload_config(N, ws, lifted=False, gather="none"):
     """The config object both arms report (same workload, same keys)."""
     rows = N
     m_total = rows * ws
+    lifted = lifted or ws > 1
+    gtxt = {"none": "", "nccl": ", C all-gathered with NCCL after the GEMM",
+            "fused": ", C all-gathered inside the GEMM epilogue (NVLink peer stores)"}[gather]
     return {"workload": f"square fp64 GEMM m=n=p={N} per GPU (BASELINE configs[1], top of the 1024-8192 sweep)"
-                        + ("" if ws == 1 else f"; row-lifted over {ws} GPUs, m={m_total}, NCCL broadcast of B each step"),
+                        + ("" if not lifted else f"; row-lifted over {ws} GPUs, m={m_total}, NCCL broadcast of B each step"
+                           + gtxt),
             "m": m_total, "n": N, "p": N, "rows_per_rank": rows,
-            "parallelism": "single GPU" if ws == 1 else f"row-lifted x{ws} (moa_gemm_lifted)",
+            "parallelism": "single GPU" if not lifted else
+            f"row-lifted x{ws} ({'moa_gemm_lifted_gather' if gather == 'fused' else 'moa_gemm_lifted'})",
+            "gather": gather,
             "l2": f"inputs larger than L2 ({(rows * N + N * N + rows * N) * 8 / 2**20:.0f} MiB resident vs 126 MB L2), no flush"}
 
 
@@ -63,6 +73,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep-sizes", default="1024,1536,2048,3072,4096,6144,8192")
+    ap.add_argument("--lifted", action="store_true",
+                    help="use the row-lifted (communicator) path even at N=1 (a 1-rank NCCL communicator)")
+    ap.add_argument("--gather", choices=["none", "nccl", "fused"], default="none",
+                    help="lifted path: also all-gather C (after the GEMM with NCCL, or fused into its epilogue)")
     return ap.parse_args()
 
 
@@ -250,10 +264,15 @@ def main():
     from inputs import inputs as I
 
     ws, rank, local = dist_env()
-    G = max(args.gpus, ws)
+    lifted = ws > 1 or args.lifted or args.gather != "none"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    if lifted:
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
 
@@ -270,13 +289,20 @@ def main():
         I.device_fill(B, 1, I.ID_B)
     else:
         B.zero_()
-    comm = moa.Comm() if ws > 1 else None
+    comm = moa.Comm() if lifted else None
+    C_full = None
+    if args.gather == "fused":
+        C_full = comm.alloc_window((m_total, p))       # NCCL symmetric window
+    elif args.gather == "nccl":
+        C_full = torch.empty((m_total, p), dtype=torch.float64, device=dev)
 
     def step():
         if comm is None:
             moa.gemm(A, B, out=C)
+        elif args.gather == "fused":
+            moa.gemm_lifted_gather(m_total, A, B, C_full, comm)
         else:
-            moa.gemm_lifted(m_total, A, B, C, comm)
+            moa.gemm_lifted(m_total, A, B, C, comm, C_full=C_full)
 
     for _ in range(args.warmup):
         step()
@@ -287,7 +313,7 @@ def main():
     idle_w = sampler.idle_watts(1.0)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws > 1:
+    if lifted:
         dist.barrier()
     torch.cuda.synchronize()
     e0 = sampler.energy_mj()
@@ -300,7 +326,7 @@ def main():
         t_end.record(stream)
         torch.cuda.synchronize()
         e1 = sampler.energy_mj()
-    if ws > 1:
+    if lifted:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     per_step = [a.elapsed_time(b) for a, b in ev]
@@ -311,9 +337,10 @@ def main():
     flops_step = 2.0 * m_total * n * p
     value = flops_step * args.steps / (elapsed_ms / 1e3) / 1e9  # GFLOP/s whole job
 
-    # dominant kernel (the GEMM itself) on the launching stream; at N > 1 the step also
-    # holds the B broadcast, so time moa_gemm alone on this rank's rows afterwards.
-    if ws > 1:
+    # dominant kernel (the GEMM itself) on the launching stream; on the lifted path the
+    # step also holds the B broadcast (and any gather), so time moa_gemm alone on this
+    # rank's rows afterwards.
+    if lifted:
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
         for a, b in kev:
             a.record(stream)
@@ -386,7 +413,8 @@ def main():
         h2d = (rows * n + (n * p if rank == 0 or ws == 1 else 0)) * 8
         e2e = {"value": round(flops_step * k_e2e / (e2e_ms / 1e3) / 1e9, 2), "unit": "GFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": rows * p * 8, "steps": k_e2e,
-               "ms_per_step": round(e2e_ms / k_e2e, 3), "api": "moa_gemm_host" if ws == 1 else "moa_gemm_lifted"}
+               "ms_per_step": round(e2e_ms / k_e2e, 3),
+               "api": "moa_gemm_host" if comm is None else "copies + moa_gemm_lifted + copy (unpipelined)"}
 
     # N sweep (GFLOP/s and J/GEMM vs N), rank 0 at N = 1 only
     sweep = None
@@ -436,11 +464,11 @@ def main():
 
     if comm is not None:
         comm.close()
-    if ws > 1:
+    if lifted:
         dist.destroy_process_group()
     if rank != 0:
         return 0
-    cfg = workload_config(N, ws)
+    cfg = workload_config(N, ws, lifted, args.gather)
     cfg["plan"] = {"kernel": plan.kernel, "bm": plan.bm, "bn": plan.bn, "bk": plan.bk, "stages": plan.stages,
                    "grid": plan.grid, "tiles": plan.tiles}
     line = {
@@ -453,6 +481,8 @@ def main():
                      "unit": "TFLOP/s", "frac": round(achieved_tf / FP64_DMMA_PEAK_TFLOPS, 4),
                      "traffic": traffic, "kernel": "k_dgemm_tma (fp64 DMMA)", "kernel_ms": round(kern_ms, 4),
                      "algorithmic_flops_per_launch": kflops, "peak_source": FP64_PEAK_SOURCE},
+        "components": {"step_ms": round(elapsed_ms / args.steps, 4), "gemm_ms": round(kern_ms, 4),
+                       "exchange_ms": round(max(0.0, elapsed_ms / args.steps - kern_ms), 4)},
         "e2e": e2e,
         "gpu_launches": args.steps,
         "energy": energy,
