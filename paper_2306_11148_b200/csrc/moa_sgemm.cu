@@ -82,14 +82,19 @@ __device__ __forceinline__ void ffma_slab(SAcc& c, const uint8_t* sA, const uint
       const int boff = k * kRowB + ((ch ^ (k & 7)) << 4);
       const float4 x = *reinterpret_cast<const float4*>(b0 + boff);
       const float4 y = *reinterpret_cast<const float4*>(b1 + boff);
+      // B pair outer, rows inner: each 64-bit B operand feeds 8 consecutive FFMA2
+      // (operand-reuse cache), the 32-bit A scalar changes. Same-box A/B against
+      // rows-outer (A reused 4x): 61.75 vs 61.32 TF/s at N=16384, identical bits
+      // (profiles/r01_ab_k3.log). Each c.v[r][q] still sees k ascending.
+      const float2 bq[4] = {make_float2(x.x, x.y), make_float2(x.z, x.w), make_float2(y.x, y.y),
+                            make_float2(y.z, y.w)};
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const float ar = kk == 0 ? a[r].x : kk == 1 ? a[r].y : kk == 2 ? a[r].z : a[r].w;
-        ffma2(c.v[r][0], ar, make_float2(x.x, x.y));
-        ffma2(c.v[r][1], ar, make_float2(x.z, x.w));
-        ffma2(c.v[r][2], ar, make_float2(y.x, y.y));
-        ffma2(c.v[r][3], ar, make_float2(y.z, y.w));
-      }
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float ar = kk == 0 ? a[r].x : kk == 1 ? a[r].y : kk == 2 ? a[r].z : a[r].w;
+          ffma2(c.v[r][q], ar, bq[q]);
+        }
     }
   }
 }

@@ -22,6 +22,7 @@ for N in (8192, 16384):
     b.record(); torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
     res[N] = round(2 * N**3 / (ms / 1e3) / 1e12, 3)
+    res["bits" + str(N)] = int(C.view(torch.int32).to(torch.int64).sum().item())  # equal bits across builds
 print(json.dumps(res))
 '''
 for rnd in range(2):
