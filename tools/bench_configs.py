@@ -26,7 +26,7 @@ import paper_2306_11148_b200 as moa  # noqa: E402
 from bench import FP64_DMMA_PEAK_TFLOPS, ClockSampler  # noqa: E402
 from inputs import inputs as I  # noqa: E402
 
-FFMA_PEAK_TFLOPS = 72.0  # measured FFMA (profiles/r01_fp64_probe.jsonl); 74.4 nominal
+FFMA_PEAK_TFLOPS = 74.0  # measured FFMA2, 16 chains/thread (profiles/r01_ffma_mix_probe.jsonl); 74.4 nominal
 TF32_NOMINAL_TFLOPS = 1100.0  # B200_PROFILING.md nominal dense TF32
 
 
