@@ -246,14 +246,34 @@ def run_reference(args):
                          "sample": f"{rows_per_step} rows x {args.steps} steps of the m=n=p={N} workload"},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
 # ----------------------------------------------------------------- GPU arm --
 
+_JSON_FD = None
+
+
+def _quiet_stdout():
+    """Route fd 1 to stderr for the whole run: native libraries (NCCL prints its
+    version banner on communicator init on some boxes) must not add lines to the ONE
+    JSON line the driver parses; emit() writes that line to the original stdout."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    sys.stdout.flush()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
     faulthandler.enable()
+    _quiet_stdout()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -391,12 +411,7 @@ def main():
             if comm is None:
                 moa.gemm_host(hA, hB, hC, A, B, C)
             else:
-                A.copy_(hA, non_blocking=True)
-                if rank == 0:
-                    B.copy_(hB, non_blocking=True)
-                moa.gemm_lifted(m_total, A, B, C, comm)
-                hC.copy_(C, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                moa.gemm_lifted_host(m_total, hA, hB if rank == 0 else None, hC, A, B, C, comm)
         e2e_step()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -414,7 +429,7 @@ def main():
         e2e = {"value": round(flops_step * k_e2e / (e2e_ms / 1e3) / 1e9, 2), "unit": "GFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": rows * p * 8, "steps": k_e2e,
                "ms_per_step": round(e2e_ms / k_e2e, 3),
-               "api": "moa_gemm_host" if comm is None else "copies + moa_gemm_lifted + copy (unpipelined)"}
+               "api": "moa_gemm_host" if comm is None else "moa_gemm_lifted_host"}
 
     # N sweep (GFLOP/s and J/GEMM vs N), rank 0 at N = 1 only
     sweep = None
@@ -490,7 +505,7 @@ def main():
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 

@@ -138,6 +138,18 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
 int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
                   void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream);
 
+/* moa_gemm_lifted_host — moa_gemm_host for the row-lifted product (COLLECTIVE):
+ * rank g's rows [row0_g, row0_g + rows_g) = moa_lift_rows(m, G, g).
+ *   A_host, C_host : rank g's rows_g x n / rows_g x p HOST rows (pinned);
+ *   B_host         : n x p HOST matrix on rank 0, ignored (may be NULL) elsewhere;
+ *   A_dev, B_dev, C_dev : device buffers of rows_g x n, n x p, rows_g x p.
+ * Same pipeline as moa_gemm_host; B's k-panels cross the host link on rank 0 only
+ * and reach every rank by one NCCL broadcast per panel on the communicator's side
+ * stream, so B's host copy, its broadcast and the first row panel's compute
+ * overlap. Synchronous. Bitwise equal to moa_gemm on the rank's rows. */
+int moa_gemm_lifted_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
+                         void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream, moa_comm_t comm);
+
 /* ------------------------------------------------------------------------
  * moa_gemm_lifted — row-lifted C := A • B over the communicator's G ranks
  * (dimension lifting of the i loop onto processors, Fig. 4

@@ -23,7 +23,7 @@ __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
     "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols", "gemm_lifted_2d", "gemm_scatter",
-    "gemm_lifted_gather",
+    "gemm_lifted_gather", "gemm_lifted_host",
 ]
 
 F64, F32, F32_3XTF32 = 0, 1, 2
@@ -60,6 +60,7 @@ def _sig(name, argtypes, restype=ctypes.c_int):
 _moa_gemm = _sig("moa_gemm", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp])
 _moa_gemm_with_plan = _sig("moa_gemm_with_plan", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, ctypes.POINTER(_PlanT), _vp])
 _moa_gemm_host = _sig("moa_gemm_host", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp])
+_moa_gemm_lifted_host = _sig("moa_gemm_lifted_host", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_lifted = _sig("moa_gemm_lifted", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_lifted_ex = _sig("moa_gemm_lifted_ex", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
 _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp])
@@ -419,6 +420,23 @@ def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precisi
                                C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
                                code, _stream_ptr(stream), comm.handle, npanels), "moa_gemm_lifted_ex")
     return C_local
+
+
+def gemm_lifted_host(m: int, A_host, B_host, C_host, A_dev, B_dev, C_dev, comm: Comm, *, stream=None):
+    """End-to-end row-lifted GEMM on HOST buffers (moa_gemm_lifted_host; collective,
+    synchronous): this rank's rows of A/C on the host, B on rank 0's host (None
+    elsewhere), device buffers for the rank's rows and all of B."""
+    n, p = B_dev.shape
+    for name, t in (("A_host", A_host), ("C_host", C_host), ("A_dev", A_dev), ("B_dev", B_dev), ("C_dev", C_dev)):
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if B_host is not None and not B_host.is_contiguous():
+        raise ValueError("B_host must be contiguous")
+    _check(_moa_gemm_lifted_host(m, n, p, A_host.data_ptr() or None,
+                                 None if B_host is None else (B_host.data_ptr() or None), C_host.data_ptr() or None,
+                                 A_dev.data_ptr() or None, B_dev.data_ptr() or None, C_dev.data_ptr() or None,
+                                 _dtype_code(B_dev), _stream_ptr(stream), comm.handle), "moa_gemm_lifted_host")
+    return C_host
 
 
 def gemm_lifted_gather(m: int, A_local, B, C_full, comm: Comm, *, stream=None, npanels: int = 0):

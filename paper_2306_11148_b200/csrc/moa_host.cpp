@@ -527,12 +527,18 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
                    (cudaStream_t)stream);
 }
 
-int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
-                  void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream) {
+// The end-to-end pipeline of moa_gemm_host; with a communicator, the rank's rows
+// of the row-lifted product (moa_gemm_lifted_host): B's k-panels cross the host
+// link on rank 0 only and reach every rank by an NCCL broadcast per panel on the
+// communicator's side stream, so the exchange of B is pipelined with the host
+// copies and with the compute of row panel 0.
+static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
+                          void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream, moa_comm_t comm) {
   int rc = validate(m, n, p, A_dev, B_dev, C_dev, dtype);
   if (rc) return rc;
   const int64_t es = elem_size(dtype);
-  if ((m * n > 0 && !A_host) || (n * p > 0 && !B_host) || (m * p > 0 && !C_host)) {
+  const bool b_root = !comm || comm->rank == 0;  // this rank reads B from the host
+  if ((m * n > 0 && !A_host) || (n * p > 0 && b_root && !B_host) || (m * p > 0 && !C_host)) {
     set_error("NULL host pointer for a non-empty operand");
     return MOA_ERR_NULL_POINTER;
   }
@@ -601,9 +607,28 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   // copy order on the H2D engine: A panel 0, B's k-panels, A panels 1..P-1
   if ((e = h2d_rows(A_host, A_dev, bnd[0], bnd[1] - bnd[0], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
   if ((e = cudaEventRecord(hp->evA[0], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  if (comm && (e = cudaStreamWaitEvent(comm->side, hp->ev0, 0)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamWaitEvent");
+  // evB[j] (the event compute waits on for B's k-panel j): after its H2D copy, or
+  // with a communicator after its broadcast from rank 0 (every processor
+  // reads all of B), issued in the same order on every rank
+  cudaEvent_t* evB = comm ? comm->ev_panel : hp->evB;
   for (int64_t j = 0; j < KB; ++j) {
-    if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
-    if ((e = cudaEventRecord(hp->evB[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if (b_root) {
+      if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
+      if ((e = cudaEventRecord(hp->evB[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    }
+    if (comm) {
+      if (b_root && (e = cudaStreamWaitEvent(comm->side, hp->evB[j], 0)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamWaitEvent");
+      if (kb[j + 1] > kb[j]) {
+        char* bp = (char*)B_dev + kb[j] * p * es;
+        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((kb[j + 1] - kb[j]) * p), nccl_type(dtype), 0, comm->nccl,
+                                       comm->side);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B panel)");
+      }
+      if ((e = cudaEventRecord(comm->ev_panel[j], comm->side)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    }
   }
   for (int64_t i = 1; i < P; ++i) {
     if ((e = h2d_rows(A_host, A_dev, bnd[i], bnd[i + 1] - bnd[i], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
@@ -612,9 +637,12 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   for (int64_t i = 0; i < P; ++i) {
     const int64_t r0 = bnd[i], rows = bnd[i + 1] - bnd[i];
     if ((e = cudaStreamWaitEvent(s, hp->evA[i], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    // (without a communicator, evA[i >= 1] follows all of B on the H2D stream)
+    if (comm && i > 0 && (e = cudaStreamWaitEvent(s, evB[KB - 1], 0)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamWaitEvent");
     if (i == 0) {
       for (int64_t j = 0; j < KB; ++j) {
-        if ((e = cudaStreamWaitEvent(s, hp->evB[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = cudaStreamWaitEvent(s, evB[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
         if (j > 0 && kb[j + 1] == kb[j]) continue;
         if ((rc = moa_gemm_acc(rows, kb[j + 1] - kb[j], p, (const char*)A_dev + (r0 * n + kb[j]) * es,
                                n > 0 ? n : 1, (const char*)B_dev + kb[j] * p * es, p > 0 ? p : 1,
@@ -635,6 +663,27 @@ int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const voi
   if ((e = cudaStreamSynchronize(hp->d2h)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(d2h)");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   return MOA_OK;
+}
+
+int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
+                  void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream) {
+  return gemm_host_impl(m, n, p, A_host, B_host, C_host, A_dev, B_dev, C_dev, dtype, stream, nullptr);
+}
+
+int moa_gemm_lifted_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
+                         void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream, moa_comm_t comm) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (m < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t row0 = 0, rows = 0;
+  int rc = moa_lift_rows(m, comm->nranks, comm->rank, &row0, &rows);
+  if (rc) return rc;
+  return gemm_host_impl(rows, n, p, A_host, B_host, C_host, A_dev, B_dev, C_dev, dtype, stream, comm);
 }
 
 int moa_comm_get_unique_id(unsigned char id[128]) {

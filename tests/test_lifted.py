@@ -275,3 +275,33 @@ def test_lifted_2d_nccl_single_rank(cuda_device):
     finally:
         comm.close()
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_lifted_host_pipeline_single_rank(cuda_device):
+    """moa_gemm_lifted_host: the e2e pipeline with B's k-panels broadcast from rank 0
+    on the communicator's side stream (1-rank NCCL: the broadcasts run, as no-ops)
+    gives moa_gemm's bits, with and without the first-panel k-chain."""
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        for (m, n, p) in [(6400, 640, 384), (300, 200, 100), (1000, 1000, 130)]:
+            A = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+            B = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+            I.device_fill(A, 4, I.ID_A)
+            I.device_fill(B, 4, I.ID_B)
+            ref = moa.gemm(A, B).cpu()
+            hA, hB = A.cpu().pin_memory(), B.cpu().pin_memory()
+            hC = torch.full((m, p), float("nan"), dtype=torch.float64).pin_memory()
+            Ad, Bd, Cd = torch.empty_like(A), torch.zeros_like(B), torch.empty((m, p), dtype=torch.float64,
+                                                                                device=cuda_device)
+            moa.gemm_lifted_host(m, hA, hB, hC, Ad, Bd, Cd, comm)
+            assert torch.equal(hC, ref), (m, n, p)
+    finally:
+        comm.close()
+        dist.destroy_process_group()
