@@ -23,4 +23,16 @@ for (m, n, p) in [(2000, 48, 2000), (7040, 16, 7040)]:
     pl = moa.plan(m, n, p)
     print(m, n, p, "float64 K1", pl.bm, pl.bn, "tiles", pl.tiles, "grid", pl.grid, "bitwise" if same else "MISMATCH")
     ok &= same
+# fused-gather epilogue (K1/K2 PEER): 3 extra destinations, stream-K and generic shapes
+for (m, n, p) in [(2000, 48, 2000), (130, 34, 66), (257, 33, 131)]:
+    A = I.host_matrix(m, n, 4, I.ID_A); B = I.host_matrix(n, p, 4, I.ID_B)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = torch.empty((m, p), dtype=torch.float64, device="cuda")
+    dst = [torch.empty((m, p), dtype=torch.float64, device="cuda") for _ in range(3)]
+    moa.gemm_scatter(Ad, Bd, C, dst)
+    torch.cuda.synchronize()
+    ref = O.ip(A, B, fused=True)
+    same = bool(np.all(C.cpu().numpy() == ref)) and all(bool(torch.equal(d, C)) for d in dst)
+    print(m, n, p, "float64 scatter x3", "bitwise" if same else "MISMATCH")
+    ok &= same
 print("ALL OK" if ok else "MISMATCH")
