@@ -234,7 +234,8 @@ int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda
  * communicator as an NCCL symmetric window (NCCL_WIN_COLL_SYMMETRIC), so every
  * rank's copy is load/store-reachable from every GPU; *ptr = this rank's copy.
  * The library owns the memory until moa_comm_free_window (COLLECTIVE) or
- * moa_comm_destroy. MOA_ERR_NCCL if not every rank is in the NVLink
+ * moa_comm_destroy; both synchronise the device first (no kernel may still be
+ * storing into a window being released). MOA_ERR_NCCL if not every rank is in the NVLink
  * load/store domain (NCCL's LSA team) or registration fails.
  * moa_comm_window_peer — *out = this process's address of rank `peer`'s copy of
  * the window byte that `ptr` addresses in this rank's copy (for peer == rank, an

@@ -1120,7 +1120,15 @@ int moa_comm_alloc_window(moa_comm_t comm, size_t bytes, void** ptr) {
     set_error("not every rank is NVLink load/store-reachable (LSA team smaller than the communicator)");
     return MOA_ERR_NCCL;
   }
-  cudaError_t e = cudaSetDevice(comm->device);
+  // allocate on the communicator's device; the caller's current device is restored
+  struct DeviceGuard {
+    int prev = -1;
+    ~DeviceGuard() {
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+  } guard;
+  cudaError_t e = cudaGetDevice(&guard.prev);
+  if (e == cudaSuccess) e = cudaSetDevice(comm->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   if (!comm->barrier_buf) {
     RelaxedCapture relaxed_capture;
