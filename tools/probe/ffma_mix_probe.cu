@@ -35,6 +35,74 @@ __global__ void k_mix(float* out, int iters, float seed) {
   if (s == 12345.678f) out[0] = s;
 }
 
+// Outer-product operand pattern of K3: 16 accumulator pairs c[r][q] (r < 8 rows,
+// q < 2 column pairs... here 8 x 2), the A scalar broadcast (.F32 operand) from 8
+// row registers and the B pair from 2 pair registers; ORDER 0 = rows outer (A reused
+// by consecutive FFMA2), 1 = B pair outer (B reused).
+template <int ORDER>
+__global__ void k_outer(float* out, int iters, float seed) {
+  unsigned long long c[8][2];
+  float a[8];
+  unsigned long long b[2];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    a[r] = seed + r * 1e-3f + threadIdx.x * 1e-6f;
+    for (int q = 0; q < 2; ++q) {
+      float2 v = make_float2((float)r, (float)q);
+      c[r][q] = *reinterpret_cast<unsigned long long*>(&v);
+    }
+  }
+  for (int q = 0; q < 2; ++q) {
+    float2 v = make_float2(seed * 0.5f + q + threadIdx.x * 1e-7f, seed * 0.25f - q - threadIdx.x * 1e-7f);
+    b[q] = *reinterpret_cast<unsigned long long*>(&v);
+  }
+  for (int it = 0; it < iters; ++it) {
+    if (ORDER == 0) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          unsigned long long aa;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a[r]));
+          asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c[r][q]) : "l"(aa), "l"(b[q]));
+        }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          unsigned long long aa;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a[r]));
+          asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c[r][q]) : "l"(aa), "l"(b[q]));
+        }
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    for (int q = 0; q < 2; ++q) s += __int_as_float((int)c[r][q]);
+  if (s == 12345.678f) out[0] = s;
+}
+
+template <int ORDER>
+void run_outer(float* out, int sms, int wps) {
+  const int iters = 20000, block = 32 * wps, grid = sms;
+  k_outer<ORDER><<<grid, block>>>(out, iters, 1.0f);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_outer<ORDER><<<grid, block>>>(out, iters, 1.0f);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double flops = 2.0 * 2.0 * 16 * iters * (double)block * grid;
+  printf("{\"probe\":\"ffma2_outer\",\"order\":\"%s\",\"warps_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.3f}\n",
+         ORDER == 0 ? "rows_outer_A_reused" : "pairs_outer_B_reused", wps, ms, flops / ms / 1e9);
+}
+
 template <int N2, int N1>
 void run(float* out, int sms, int wps) {
   const int iters = 20000, block = 32 * wps, grid = sms;
@@ -59,6 +127,10 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* out;
   cudaMalloc(&out, 16);
+  for (int wps : {8, 16}) {
+    run_outer<0>(out, sms, wps);
+    run_outer<1>(out, sms, wps);
+  }
   for (int wps : {8, 16, 32}) {
     run<8, 0>(out, sms, wps);
     run<0, 16>(out, sms, wps);
