@@ -241,21 +241,33 @@ int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* 
   for (int i = 0; i < nc; ++i) {
     const TileConfig& c = cfgs[i];
     if (c.smem_bytes > ds.smem_optin) continue;
+    double eta = c.eta;
+    if (eta <= 0.0) {
+      // A 32-column tile (K1 64x32) is offered only where every 64-column tile would
+      // waste columns (p mod 64 in (0, 32]): thin-p shapes, e.g. m = 2^20, n = p = 32,
+      // where 128x64 does twice the DMMA work (177 vs 90.6 us; 64x32 reaches 5.9 TB/s,
+      // 91% of HBM: profiles/r01_skinny_hbm.jsonl). Its eta there is its large-N
+      // efficiency relative to 128x128 (N=2048: 0.95), so near-square shapes keep the
+      // wide tiles.
+      const int64_t c32 = (p + 31) / 32 * 32, c64 = (p + 63) / 64 * 64;
+      if (!(c.kernel == MOA_KERNEL_DGEMM_TMA && c.bn == 32 && c.bm * c.bn > 32 * 32 && c32 < c64)) continue;
+      eta = 0.95;
+    }
     const int64_t tm = (m + c.bm - 1) / c.bm, tn = (p + c.bn - 1) / c.bn, tiles = tm * tn;
     const int64_t waves = (tiles + ds.sms - 1) / ds.sms;
-    double eff = (double)m * (double)p / ((double)waves * ds.sms * (double)c.bm * c.bn) * c.eta;
+    double eff = (double)m * (double)p / ((double)waves * ds.sms * (double)c.bm * c.bn) * eta;
     if (c.kernel == MOA_KERNEL_DGEMM_TMA && (int64_t)c.bm * c.bn <= 32 * 32) {
       // Latency tiles (16x16 outputs per warp, one resident CTA per tile): only for
       // tiny problems (fewer 64x32 tiles than SMs), where the time is the longest
       // DMMA chain per SM sub-partition: ceil(warps / (4 SMs)) warps of 16x16 each.
       if ((double)m * (double)p >= (double)ds.sms * 64.0 * 32.0) continue;
       const int64_t warps = tiles * ((int64_t)c.bm * c.bn / 256), smsp = 4LL * ds.sms;
-      eff = (double)m * (double)p / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * c.eta;
+      eff = (double)m * (double)p / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * eta;
     }
     // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
     // cut tiles cost a partial store + reload and an extra pipeline fill: -1%.
     if (c.kernel == MOA_KERNEL_DGEMM_TMA && use_stream_k(tiles, grid_for(c.kernel, tiles, ds.sms, c.ctas_per_sm, (int64_t)c.bm * c.bn)))
-      eff = (double)m * (double)p / ((double)tiles * c.bm * c.bn) * c.eta * 0.99;
+      eff = (double)m * (double)p / ((double)tiles * c.bm * c.bn) * eta * 0.99;
     if (eff > best + 1e-12) {
       best = eff;
       bi = i;

@@ -224,6 +224,12 @@ def test_plan_is_static_and_sane(cuda_device):
         assert moa.plan(m, n, p) == pl
     assert moa.plan(16384, 16384, 16384).bm == 128
     assert moa.plan(5, 7, 9).kernel == "dgemm_generic"  # odd n / p: not describable by TMA
+    # thin p (the HBM-bound diagnostic m = 2^20, n = p = 32): a 32-column tile, no
+    # wasted DMMA columns; near-square shapes keep the wide tiles
+    for (m, n, p) in [(1 << 20, 32, 32), (1 << 20, 16, 16), (1 << 18, 128, 32), (1 << 20, 96, 96)]:
+        assert moa.plan(m, n, p).bn == 32, (m, n, p)
+    for (m, n, p) in [(8224, 8224, 8224), (1 << 20, 64, 64), (4096, 4096, 4096)]:
+        assert moa.plan(m, n, p).bn >= 64, (m, n, p)
 
 
 def _freivalds(Ct, tA, tB, trials=2):
