@@ -225,7 +225,7 @@ int32_t grid_for(int kernel, int64_t tiles, int sms, int ctas_per_sm, int64_t ti
 // for the K1 latency tiles, tiny problems only: the longest chain per SM sub-partition),
 // i.e. the lifted block (bm x bn) "as close as possible" to filling every SM's
 // fp64 pipe for a whole number of waves. No measurement, no autotuning.
-int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* out) {
+int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, moa_plan_t* out) {
   const TileConfig* cfgs = nullptr;
   int nc = 0;
   if (kernel == MOA_KERNEL_DGEMM_TMA || kernel == MOA_KERNEL_DGEMM_GENERIC)
@@ -265,9 +265,18 @@ int choose(int kernel, int64_t m, int64_t p, const DeviceShape& ds, moa_plan_t* 
       eff = (double)m * (double)p / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * eta;
     }
     // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
-    // cut tiles cost a partial store + reload and an extra pipeline fill: -1%.
-    if (c.kernel == MOA_KERNEL_DGEMM_TMA && use_stream_k(tiles, grid_for(c.kernel, tiles, ds.sms, c.ctas_per_sm, (int64_t)c.bm * c.bn)))
-      eff = (double)m * (double)p / ((double)tiles * c.bm * c.bn) * eta * 0.99;
+    // cut tiles cost a partial store + reload and an extra pipeline fill: -1%, and
+    // each run of R k-slabs pays about 4 slabs of hand-off, which only matters for
+    // shallow k (n = 64: R ~ 7 slabs; 256x64x8192 took 19.3 us with 128x64 stream-K
+    // vs 14.2 us with one wave of 128x128 tiles).
+    const int32_t grid = grid_for(c.kernel, tiles, ds.sms, c.ctas_per_sm, (int64_t)c.bm * c.bn);
+    if (c.kernel == MOA_KERNEL_DGEMM_TMA && use_stream_k(tiles, grid)) {
+      const double run = (double)tiles * (double)((n + c.bk - 1) / c.bk) / (double)grid;
+      eff = (double)m * (double)p / ((double)tiles * c.bm * c.bn) * eta * 0.99 * run / (run + 4.0);
+      // a 4-warp 64x32 CTA alone on an SM (stream-K grid = SMs) leaves one warp per
+      // sub-partition: N = 1024 ran 98 vs 72 us with the same tiles two-plus per SM
+      if (grid <= ds.sms && (int64_t)c.bm * c.bn <= 64 * 32) eff *= 0.75;
+    }
     if (eff > best + 1e-12) {
       best = eff;
       bi = i;
@@ -315,7 +324,7 @@ int plan_impl(int64_t m, int64_t n, int64_t p, int dtype, const DeviceShape& ds,
     set_error("unknown dtype");
     return MOA_ERR_INVALID_DTYPE;
   }
-  return choose(kernel, m, p, ds, out);
+  return choose(kernel, m, n, p, ds, out);
 }
 
 int check_device(const DeviceShape& ds) {
