@@ -21,6 +21,7 @@
 // Library-owned communicator: the NCCL communicator plus a side stream and events
 // used to pipeline the broadcast of B's k-panels against the lifted compute.
 constexpr int kMaxPanels = 16;
+constexpr int kPipeCTAs = 4;
 struct moa_comm_s {
   ncclComm_t nccl = nullptr;
   int nranks = 0;
@@ -32,6 +33,10 @@ struct moa_comm_s {
   // 2-D lifting: row / column sub-communicators for the last grid shape used
   int grid_rows = 0, grid_cols = 0;
   ncclComm_t row_comm = nullptr, col_comm = nullptr;
+  // Pipelined B panels (after the first) travel on a split of the communicator whose
+  // kernels are limited to kPipeCTAs CTAs; the GEMMs they overlap leave that many
+  // SMs free (see gemm_reserving).
+  ncclComm_t pipe = nullptr;
   // Symmetric windows (moa_comm_alloc_window) for the fused GEMM -> all-gather:
   // ncclMemAlloc'd memory registered on this communicator, with every rank's copy
   // resolved to an address in this process.
@@ -548,6 +553,9 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
                    (cudaStream_t)stream);
 }
 
+static int gemm_reserving(const GemmArgs& g, int dtype, cudaStream_t s, int reserve);
+static int pipe_comm(moa_comm_t comm, ncclComm_t* out);
+
 // The end-to-end pipeline of moa_gemm_host; with a communicator, the rank's rows
 // of the row-lifted product (moa_gemm_lifted_host): B's k-panels cross the host
 // link on rank 0 only and reach every rank by an NCCL broadcast per panel on the
@@ -634,6 +642,8 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
   // with a communicator after its broadcast from rank 0 (every processor
   // reads all of B), issued in the same order on every rank
   cudaEvent_t* evB = comm ? comm->ev_panel : hp->evB;
+  ncclComm_t pipe = nullptr;  // panels after the first overlap GEMMs: CTA-limited comm
+  if (comm && KB > 1 && (rc = pipe_comm(comm, &pipe))) return rc;
   for (int64_t j = 0; j < KB; ++j) {
     if (b_root) {
       if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
@@ -644,8 +654,8 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
         return cuda_fail(e, "cudaStreamWaitEvent");
       if (kb[j + 1] > kb[j]) {
         char* bp = (char*)B_dev + kb[j] * p * es;
-        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((kb[j + 1] - kb[j]) * p), nccl_type(dtype), 0, comm->nccl,
-                                       comm->side);
+        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((kb[j + 1] - kb[j]) * p), nccl_type(dtype), 0,
+                                       j == 0 ? comm->nccl : pipe, comm->side);
         if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B panel)");
       }
       if ((e = cudaEventRecord(comm->ev_panel[j], comm->side)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
@@ -665,10 +675,10 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
       for (int64_t j = 0; j < KB; ++j) {
         if ((e = cudaStreamWaitEvent(s, evB[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
         if (j > 0 && kb[j + 1] == kb[j]) continue;
-        if ((rc = moa_gemm_acc(rows, kb[j + 1] - kb[j], p, (const char*)A_dev + (r0 * n + kb[j]) * es,
-                               n > 0 ? n : 1, (const char*)B_dev + kb[j] * p * es, p > 0 ? p : 1,
-                               (char*)C_dev + r0 * p * es, p > 0 ? p : 1, j > 0 ? 1 : 0, dtype, stream)))
-          return rc;
+        const GemmArgs g{rows, kb[j + 1] - kb[j], p, (const char*)A_dev + (r0 * n + kb[j]) * es, (const char*)B_dev + kb[j] * p * es,
+                         (char*)C_dev + r0 * p * es, n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
+        // with a communicator, later B panels are still being broadcast: leave SMs free
+        if ((rc = gemm_reserving(g, dtype, s, comm && j < KB - 1 ? kPipeCTAs : 0))) return rc;
       }
     } else if ((rc = moa_gemm(rows, n, p, (const char*)A_dev + r0 * n * es, B_dev, (char*)C_dev + r0 * p * es, dtype,
                               stream))) {
@@ -762,6 +772,7 @@ int moa_comm_destroy(moa_comm_t comm) {
   if (!comm) return MOA_OK;
   if (comm->row_comm) ncclCommDestroy(comm->row_comm);
   if (comm->col_comm) ncclCommDestroy(comm->col_comm);
+  if (comm->pipe) ncclCommDestroy(comm->pipe);
   if (comm->side) cudaStreamSynchronize(comm->side);
   for (auto& w : comm->windows) {
     cudaDeviceSynchronize();  // no kernel may still be storing into the window
@@ -850,6 +861,47 @@ int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks) {
   return k < 1 ? 1 : (int)k;
 }
 
+// A GEMM that leaves `reserve` SMs free for a concurrent collective. A persistent
+// K1 grid takes every SM's registers and shared memory (one 384-thread CTA with
+// 168..232 registers per thread and ~193 KiB of smem), so an NCCL kernel launched
+// next to it could not start until the GEMM had ended: the "overlapped" broadcast
+// would in fact serialise. The pipe communicator's kernels use at most kPipeCTAs
+// CTAs, and this GEMM's grid is capped at (SMs - reserve) x CTAs-per-SM. Every
+// kernel's work assignment is grid-size independent (persistent tile loops, and
+// stream-K runs of R >= K slabs since tiles >= grid), so the result is unchanged.
+static int gemm_reserving(const GemmArgs& g, int dtype, cudaStream_t s, int reserve) {
+  int rc = validate_g(g, dtype);
+  if (rc) return rc;
+  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64) {
+    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 only");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  DeviceShape ds;
+  if ((rc = get_device_shape(-1, &ds)) || (rc = check_device(ds))) return rc;
+  moa_plan_t pl;
+  if ((rc = plan_impl(g.m, g.n, g.p, dtype, ds, tma_eligible(g, elem_size(dtype)), &pl))) return rc;
+  if (reserve > 0 && pl.grid > 0 && ds.sms > reserve) {
+    const int64_t cap = (int64_t)(ds.sms - reserve) * (pl.ctas_per_sm > 0 ? pl.ctas_per_sm : 1);
+    if (pl.grid > cap) pl.grid = (int32_t)cap;
+  }
+  return run_plan(pl, g, dtype, s);
+}
+
+static int pipe_comm(moa_comm_t comm, ncclComm_t* out) {
+  if (!comm->pipe) {
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.minCTAs = 1;
+    cfg.maxCTAs = kPipeCTAs;
+    ncclResult_t r = ncclCommSplit(comm->nccl, 0, comm->rank, &comm->pipe, &cfg);
+    if (r != ncclSuccess) {
+      comm->pipe = nullptr;
+      return nccl_fail(r, "ncclCommSplit(pipe)");
+    }
+  }
+  *out = comm->pipe;
+  return MOA_OK;
+}
+
 // Steps (1)-(2) of the row-lifted GEMM, shared by moa_gemm_lifted_ex and
 // moa_gemm_lifted_gather: the broadcast of B (optionally pipelined in k-panels) and
 // this rank's rows of C. `last_peers` (fused gather) goes to the launch that writes
@@ -870,7 +922,7 @@ static int lifted_bcast_compute(int64_t n, int64_t p, int64_t rows, const void* 
     int64_t b = (n * j / K) / 32 * 32;
     bnd[j] = j == K ? n : b;
   }
-  if (K == 1 || comm->nranks == 1) {
+  if (K == 1) {
     // (1) every processor needs all of B (ip_rows.c reads B[(sigma*sizer)+j] with no
     //     processor index): in-place broadcast from rank 0 over NVLink.
     if (n * p > 0 && comm->nranks > 1) {
@@ -879,14 +931,20 @@ static int lifted_bcast_compute(int64_t n, int64_t p, int64_t rows, const void* 
     }
   } else {
     // Pipelined exchange (NEXT-1 step 1): broadcast the k-panels of B on the side
-    // stream, each followed by an event the compute stream waits on.
+    // stream, each followed by an event the compute stream waits on. Panel 0 goes
+    // first on the full communicator (nothing computes yet); the later panels go on
+    // the CTA-limited pipe communicator while the panel GEMMs leave kPipeCTAs SMs
+    // free for them (gemm_reserving). With one rank the broadcasts are no-ops but
+    // run the same path.
+    ncclComm_t pipe = nullptr;
+    if ((rc = pipe_comm(comm, &pipe))) return rc;
     if ((e = cudaEventRecord(comm->ev_start, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     if ((e = cudaStreamWaitEvent(comm->side, comm->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     for (int j = 0; j < K; ++j) {
       const int64_t k0 = bnd[j], k1 = bnd[j + 1];
       if (k1 > k0) {
         char* bp = (char*)B + k0 * p * es;
-        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((k1 - k0) * p), ty, 0, comm->nccl, comm->side);
+        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((k1 - k0) * p), ty, 0, j == 0 ? comm->nccl : pipe, comm->side);
         if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B panel)");
       }
       if ((e = cudaEventRecord(comm->ev_panel[j], comm->side)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
@@ -898,13 +956,14 @@ static int lifted_bcast_compute(int64_t n, int64_t p, int64_t rows, const void* 
   //     blocks").
   for (int j = 0; j < K; ++j) {
     const int64_t k0 = bnd[j], k1 = bnd[j + 1];
-    if (K > 1 && comm->nranks > 1)
+    if (K > 1)
       if ((e = cudaStreamWaitEvent(s, comm->ev_panel[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     if (k1 <= k0 && j > 0) continue;
     GemmArgs g{rows, k1 - k0, p, (const char*)A_local + k0 * es, (const char*)B + k0 * p * es, C_local,
                n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
     if (j == K - 1) g.peers = last_peers;  // the final panel writes the final C
-    if ((rc = gemm_impl(g, dtype, nullptr, s))) return rc;
+    // panels that run while later panels are still being broadcast leave SMs free
+    if ((rc = gemm_reserving(g, dtype, s, j < K - 1 ? kPipeCTAs : 0))) return rc;
   }
   return MOA_OK;
 }
