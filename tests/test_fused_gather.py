@@ -177,3 +177,47 @@ def test_lifted_gather_single_rank_nccl(cuda_device):
     finally:
         comm.close()
         dist.destroy_process_group()
+
+
+def _ipc_worker(rank, world, m, n, p, q_out, q_in, barrier, result):
+    """One 'rank' of a two-process gather on one GPU: its C_full travels to the other
+    process by CUDA IPC, and each process's epilogue stores its rows into both copies
+    (the address arithmetic of moa_gemm_lifted_gather, with IPC standing in for the
+    NCCL window's NVLink mapping)."""
+    import torch
+    import numpy as np
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    from oracle import oracle as O
+    dev = torch.device("cuda:0")
+    row0, rows = moa.lift_rows(m, world, rank)
+    C_full = torch.full((m, p), float("nan"), dtype=torch.float64, device=dev)
+    q_out.put(C_full)                      # CUDA IPC handle to the peer
+    peer = q_in.get(timeout=120)           # the peer's C_full, mapped here
+    A = torch.from_numpy(I.host_matrix(rows, n, 5, I.ID_A, row0=row0)).to(dev)
+    B = torch.from_numpy(I.host_matrix(n, p, 5, I.ID_B)).to(dev)
+    barrier.wait()                         # entry barrier: both copies allocated and initialised
+    moa.gemm_scatter(A, B, C_full[row0:row0 + rows], [peer[row0:row0 + rows].data_ptr()])
+    torch.cuda.synchronize()
+    barrier.wait()                         # exit barrier: both epilogues complete
+    ref = O.ip(I.host_matrix(m, n, 5, I.ID_A), I.host_matrix(n, p, 5, I.ID_B), fused=True)
+    result.put((rank, bool(np.array_equal(C_full.cpu().numpy(), ref))))
+    barrier.wait()                         # keep our C_full alive until the peer has checked
+
+
+@pytest.mark.gpu
+def test_scatter_two_process_gather_over_cuda_ipc(cuda_device):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    m, n, p = 1000, 96, 520                # G = 2: rows 500 + 500, ragged tile edges
+    q01, q10, res = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    bar = ctx.Barrier(2)
+    procs = [ctx.Process(target=_ipc_worker, args=(0, 2, m, n, p, q01, q10, bar, res)),
+             ctx.Process(target=_ipc_worker, args=(1, 2, m, n, p, q10, q01, bar, res))]
+    for pr in procs:
+        pr.start()
+    out = dict(res.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    assert out == {0: True, 1: True}
