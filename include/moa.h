@@ -138,7 +138,9 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
 int moa_gemm_host(int64_t m, int64_t n, int64_t p, const void* A_host, const void* B_host, void* C_host,
                   void* A_dev, void* B_dev, void* C_dev, int dtype, void* stream);
 
-/* moa_gemm_lifted_host — moa_gemm_host for the row-lifted product (COLLECTIVE):
+/* moa_gemm_lifted_host — moa_gemm_host for the row-lifted product (COLLECTIVE;
+ * dimension lifting of the i loop, Fig. 4 ip_rows.c P:150-171; every
+ * processor reads all of B, P:165 / reading R13):
  * rank g's rows [row0_g, row0_g + rows_g) = moa_lift_rows(m, G, g).
  *   A_host, C_host : rank g's rows_g x n / rows_g x p HOST rows (pinned);
  *   B_host         : n x p HOST matrix on rank 0, ignored (may be NULL) elsewhere;
@@ -211,7 +213,10 @@ int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_
 
 /* ------------------------------------------------------------------------
  * The row-lifted GEMM with the all-gather of C FUSED into the GEMM (SURVEY §8(f)
- * NEXT-1 step 3; reading R14: every rank ends with all of C). Instead of a GEMM
+ * NEXT-1 step 3). Rows of C depend only on the same rows of A and all of B (Fig. 1,
+ * P:90-99), so rank g's rows (Fig. 4 ip_rows.c P:150-171) are final as
+ * soon as its tiles are; the gather (reading R14: every rank ends with all of C)
+ * only places them. Instead of a GEMM
  * followed by ncclAllGather, the epilogue of the GEMM kernel stores every final C
  * tile of rank g's rows [row0_g, row0_g + rows_g) both into its own C_full and,
  * over NVLink, into every other rank's C_full at the same rows — so the exchange
