@@ -194,6 +194,11 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
  *   C_local : device, m x cols_g, receives rank g's column block of C.
  *   C_full  : NULL, or device m x p receiving all of C on every rank; then
  *   workspace must hold m * ceil(p / G) elements (not needed when G == 1).
+ *   If C_full lies inside a window from moa_comm_alloc_window and dtype is
+ *   MOA_F64, the gather is fused into the GEMM epilogue instead (each rank's
+ *   column block is computed into its columns of C_full, row stride p, and stored
+ *   by the same epilogue into every peer's C_full; entry/exit barriers as in
+ *   moa_gemm_lifted_gather); workspace is then unused.
  * Bitwise identical to moa_gemm on one GPU (the k order of every element is
  * unchanged by a j split). */
 int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,

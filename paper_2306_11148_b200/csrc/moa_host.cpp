@@ -1030,6 +1030,9 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
   return MOA_OK;
 }
 
+static const moa_comm_s::Window* find_window(moa_comm_t comm, const void* ptr, int64_t bytes);
+static int stream_barrier(moa_comm_t comm, cudaStream_t s);
+
 int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,
                          void* workspace, int dtype, void* stream, moa_comm_t comm) {
   if (!comm) {
@@ -1045,7 +1048,14 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
   if (rc) return rc;
   if ((rc = validate(m, n, cols, A, B_local, C_local, dtype))) return rc;
   const int64_t es = elem_size(dtype);
-  if (C_full && m * p > 0) {
+  // C_full inside a symmetric window (moa_comm_alloc_window), fp64: the gather is fused
+  // into the GEMM epilogue — this rank's column block is computed straight into its
+  // columns of C_full (row stride p) and stored by the same epilogue into every
+  // peer's C_full over NVLink; no workspace, no per-rank broadcasts of C.
+  const moa_comm_s::Window* win =
+      (C_full && m * p > 0 && dtype == MOA_F64 && comm->nranks - 1 <= kMaxPeerDst) ? find_window(comm, C_full, m * p * es)
+                                                                                  : nullptr;
+  if (C_full && m * p > 0 && !win) {
     if ((reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
       set_error("C_full not aligned to the element size");
       return MOA_ERR_MISALIGNED;
@@ -1062,6 +1072,26 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
   if (m * n > 0 && comm->nranks > 1) {
     ncclResult_t r = ncclBroadcast(A, A, (size_t)(m * n), ty, 0, comm->nccl, s);
     if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(A)");
+  }
+  if (win) {
+    if ((rc = stream_barrier(comm, s))) return rc;  // entry: every rank reached this call
+    if (m * n > 0 && comm->nranks > 1) {
+      ncclResult_t r = ncclBroadcast(A, A, (size_t)(m * n), ty, 0, comm->nccl, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(A)");
+    }
+    PeerDst pd{};
+    const uintptr_t off = (uintptr_t)C_full - (uintptr_t)win->ptr + (uintptr_t)(col0 * es);
+    for (int r = 0; r < comm->nranks; ++r)
+      if (r != comm->rank && cols > 0) pd.dst[pd.nd++] = (char*)win->peer[(size_t)r] + off;
+    GemmArgs g{m, n, cols, A, B_local, (char*)C_full + col0 * es, n > 0 ? n : 1, cols > 0 ? cols : 1, p, 0};
+    g.peers = &pd;
+    if (cols > 0 && (rc = gemm_impl(g, dtype, nullptr, s))) return rc;
+    if (m * cols > 0) {  // C_local receives the block as documented (local strided copy)
+      cudaError_t e = cudaMemcpy2DAsync(C_local, (size_t)(cols * es), (const char*)C_full + col0 * es, (size_t)(p * es),
+                                        (size_t)(cols * es), (size_t)m, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_local)");
+    }
+    return stream_barrier(comm, s);  // exit: every rank's epilogue stores are complete
   }
   // (2) this rank's column block: C[:, col0:col0+cols] = A • B[:, col0:col0+cols].
   if ((rc = moa_gemm(m, n, cols, A, B_local, C_local, dtype, stream))) return rc;
@@ -1279,6 +1309,15 @@ int moa_comm_window_peer(moa_comm_t comm, const void* ptr, int peer, void** out)
   return MOA_ERR_NOT_REGISTERED;
 }
 
+// The window (moa_comm_alloc_window) holding [ptr, ptr + bytes), or nullptr.
+static const moa_comm_s::Window* find_window(moa_comm_t comm, const void* ptr, int64_t bytes) {
+  for (const auto& w : comm->windows) {
+    const uintptr_t a = (uintptr_t)ptr, b = (uintptr_t)w.ptr;
+    if (a >= b && a + (uintptr_t)bytes <= b + w.bytes) return &w;
+  }
+  return nullptr;
+}
+
 // Barrier of the fused gather: a one-element all-reduce on the stream. When it
 // completes on rank r, every rank has finished the work it enqueued before it (for
 // the exit barrier: its GEMM, whose peer stores are complete at kernel end).
@@ -1326,10 +1365,7 @@ int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local,
       set_error("NULL C_full");
       return MOA_ERR_NULL_POINTER;
     }
-    for (const auto& w : comm->windows) {
-      const uintptr_t a = (uintptr_t)C_full, b = (uintptr_t)w.ptr;
-      if (a >= b && a + (uintptr_t)mp <= b + w.bytes) win = &w;
-    }
+    win = find_window(comm, C_full, mp);
     if (!win) {
       set_error("C_full is not inside a window from moa_comm_alloc_window (of m*p elements)");
       return MOA_ERR_NOT_REGISTERED;

@@ -221,3 +221,29 @@ def test_scatter_two_process_gather_over_cuda_ipc(cuda_device):
         pr.join(timeout=120)
         assert pr.exitcode == 0
     assert out == {0: True, 1: True}
+
+
+@pytest.mark.gpu
+def test_lifted_cols_fused_gather_single_rank(cuda_device):
+    """Column lifting (Fig. 5 ip_cols.c at GPU level) with C_full in a symmetric window:
+    the column block is computed straight into C_full's columns (row stride p) by the
+    PEER epilogue path, no workspace; C_full and C_local bitwise moa_gemm."""
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    comm = moa.Comm(device=0)
+    try:
+        for (m, n, p) in [(1000, 256, 300), (2000, 48, 2000), (257, 33, 131)]:
+            A, B = _operands(m, n, p, 11, cuda_device)
+            ref = moa.gemm(A, B)
+            C_full = comm.alloc_window((m, p))
+            C_full.fill_(float("nan"))
+            C_local = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+            moa.gemm_lifted_cols(A, B, C_local, p, comm, C_full=C_full)
+            torch.cuda.synchronize()
+            assert torch.equal(C_full, ref) and torch.equal(C_local, ref), (m, n, p)
+            comm.free_window(C_full)
+    finally:
+        comm.close()
+        dist.destroy_process_group()
