@@ -216,6 +216,16 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
 int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
                        void* C_block, int dtype, void* stream, moa_comm_t comm);
 
+/* moa_gemm_lifted_2d_gather — moa_gemm_lifted_2d with the all-gather of C fused into
+ * the GEMM epilogue (as moa_gemm_lifted_gather): C_full (m x p, inside a window from
+ * moa_comm_alloc_window on every rank; MOA_ERR_NOT_REGISTERED otherwise) receives
+ * all of C on every rank. Rank (r, c) computes its block straight into C_full at
+ * rows [row0_r, row0_r + rows_r) x columns [col0_c, col0_c + cols_c) (row stride p);
+ * the same epilogue stores it into every other rank's C_full; C_block also receives
+ * the block. Entry/exit barriers as moa_gemm_lifted_gather. MOA_F64 only. */
+int moa_gemm_lifted_2d_gather(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel,
+                              void* B_panel, void* C_block, void* C_full, int dtype, void* stream, moa_comm_t comm);
+
 /* ------------------------------------------------------------------------
  * The row-lifted GEMM with the all-gather of C FUSED into the GEMM (SURVEY §8(f)
  * NEXT-1 step 3). Rows of C depend only on the same rows of A and all of B (Fig. 1,

@@ -67,6 +67,8 @@ _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _v
 _moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
 _moa_gemm_lifted_cols = _sig("moa_gemm_lifted_cols", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_lifted_2d = _sig("moa_gemm_lifted_2d", [_i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp])
+_moa_gemm_lifted_2d_gather = _sig("moa_gemm_lifted_2d_gather", [_i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _i32,
+                                                                _vp, _vp])
 _moa_gemm_scatter = _sig("moa_gemm_scatter", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32,
                                               ctypes.POINTER(_vp), _i32, _vp])
 _moa_gemm_lifted_gather = _sig("moa_gemm_lifted_gather", [_i64, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
@@ -492,13 +494,21 @@ def gemm_lifted_cols(A, B_local, C_local, p: int, comm: Comm, C_full=None, works
 
 
 def gemm_lifted_2d(m: int, p: int, grid_rows: int, grid_cols: int, A_panel, B_panel, C_block, comm: Comm, *,
-                   stream=None):
-    """2-D lifted C := A • B on a grid_rows x grid_cols process grid (moa_gemm_lifted_2d)."""
+                   C_full=None, stream=None):
+    """2-D lifted C := A • B on a grid_rows x grid_cols process grid (moa_gemm_lifted_2d);
+    with C_full (a comm.alloc_window tensor) the all-gather of C is fused into the GEMM
+    epilogue (moa_gemm_lifted_2d_gather)."""
     n = A_panel.shape[1]
     code = _dtype_code(A_panel)
     for name, t in (("A_panel", A_panel), ("B_panel", B_panel), ("C_block", C_block)):
         if not t.is_cuda or not t.is_contiguous():
             raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    if C_full is not None:
+        _check(_moa_gemm_lifted_2d_gather(m, n, p, grid_rows, grid_cols, A_panel.data_ptr() or None,
+                                          B_panel.data_ptr() or None, C_block.data_ptr() or None,
+                                          C_full.data_ptr() or None, code, _stream_ptr(stream), comm.handle),
+               "moa_gemm_lifted_2d_gather")
+        return C_block
     _check(_moa_gemm_lifted_2d(m, n, p, grid_rows, grid_cols, A_panel.data_ptr() or None, B_panel.data_ptr() or None,
                                C_block.data_ptr() or None, code, _stream_ptr(stream), comm.handle),
            "moa_gemm_lifted_2d")

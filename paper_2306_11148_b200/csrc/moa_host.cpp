@@ -1117,8 +1117,8 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
   return MOA_OK;
 }
 
-int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
-                       void* C_block, int dtype, void* stream, moa_comm_t comm) {
+static int lifted_2d_impl(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel,
+                          void* B_panel, void* C_block, void* C_full, int dtype, void* stream, moa_comm_t comm) {
   if (!comm) {
     set_error("NULL communicator");
     return MOA_ERR_NULL_POINTER;
@@ -1133,8 +1133,25 @@ int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_
   if (!rc) rc = moa_lift_rows(p, grid_cols, c, &col0, &cols);
   if (rc) return rc;
   if ((rc = validate(rows, n, cols, A_panel, B_panel, C_block, dtype))) return rc;
+  const int64_t es = elem_size(dtype);
+  const moa_comm_s::Window* win = nullptr;
+  if (C_full && m * p > 0) {  // the fused gather: C_full must be a symmetric window, fp64
+    if (dtype != MOA_F64) {
+      set_error("moa_gemm_lifted_2d_gather: MOA_F64 only");
+      return MOA_ERR_INVALID_DTYPE;
+    }
+    if (comm->nranks - 1 > kMaxPeerDst) {
+      set_error("moa_gemm_lifted_2d_gather: at most 9 ranks (one NVLink node)");
+      return MOA_ERR_INVALID_SHAPE;
+    }
+    if (!(win = find_window(comm, C_full, m * p * es))) {
+      set_error("C_full is not inside a window from moa_comm_alloc_window (of m*p elements)");
+      return MOA_ERR_NOT_REGISTERED;
+    }
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const ncclDataType_t ty = nccl_type(dtype);
+  if (win && (rc = stream_barrier(comm, s))) return rc;  // entry: every rank reached this call
   if (comm->nranks > 1) {
     if (comm->grid_rows != grid_rows || comm->grid_cols != grid_cols) {  // (re)split, collective
       if (comm->row_comm) ncclCommDestroy(comm->row_comm);
@@ -1155,7 +1172,37 @@ int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_
       q = ncclBroadcast(B_panel, B_panel, (size_t)(n * cols), ty, 0, comm->col_comm, s);
     if (q != ncclSuccess) return nccl_fail(q, "ncclBroadcast(2-D panels)");
   }
-  return moa_gemm(rows, n, cols, A_panel, B_panel, C_block, dtype, stream);
+  if (!win) return moa_gemm(rows, n, cols, A_panel, B_panel, C_block, dtype, stream);
+  // fused gather: the block is computed into C_full at (row0, col0) with row stride p
+  // and stored by the same epilogue into every other rank's C_full at that offset
+  PeerDst pd{};
+  const uintptr_t off = (uintptr_t)C_full - (uintptr_t)win->ptr + (uintptr_t)((row0 * p + col0) * es);
+  for (int q = 0; q < comm->nranks; ++q)
+    if (q != comm->rank && rows * cols > 0) pd.dst[pd.nd++] = (char*)win->peer[(size_t)q] + off;
+  GemmArgs g{rows, n, cols, A_panel, B_panel, (char*)C_full + (row0 * p + col0) * es, n > 0 ? n : 1,
+             cols > 0 ? cols : 1, p, 0};
+  g.peers = &pd;
+  if (rows * cols > 0 && (rc = gemm_impl(g, dtype, nullptr, s))) return rc;
+  if (rows * cols > 0) {
+    cudaError_t e = cudaMemcpy2DAsync(C_block, (size_t)(cols * es), (const char*)C_full + (row0 * p + col0) * es,
+                                      (size_t)(p * es), (size_t)(cols * es), (size_t)rows, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_block)");
+  }
+  return stream_barrier(comm, s);  // exit: every rank's epilogue stores are complete
+}
+
+int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
+                       void* C_block, int dtype, void* stream, moa_comm_t comm) {
+  return lifted_2d_impl(m, n, p, grid_rows, grid_cols, A_panel, B_panel, C_block, nullptr, dtype, stream, comm);
+}
+
+int moa_gemm_lifted_2d_gather(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel,
+                              void* B_panel, void* C_block, void* C_full, int dtype, void* stream, moa_comm_t comm) {
+  if (comm && m * p > 0 && !C_full) {
+    set_error("NULL C_full");
+    return MOA_ERR_NULL_POINTER;
+  }
+  return lifted_2d_impl(m, n, p, grid_rows, grid_cols, A_panel, B_panel, C_block, C_full, dtype, stream, comm);
 }
 
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,

@@ -224,7 +224,7 @@ def test_scatter_two_process_gather_over_cuda_ipc(cuda_device):
 
 
 @pytest.mark.gpu
-def test_lifted_cols_fused_gather_single_rank(cuda_device):
+def test_lifted_cols_and_2d_fused_gather_single_rank(cuda_device):
     """Column lifting (Fig. 5 ip_cols.c at GPU level) with C_full in a symmetric window:
     the column block is computed straight into C_full's columns (row stride p) by the
     PEER epilogue path, no workspace; C_full and C_local bitwise moa_gemm."""
@@ -243,6 +243,12 @@ def test_lifted_cols_fused_gather_single_rank(cuda_device):
             moa.gemm_lifted_cols(A, B, C_local, p, comm, C_full=C_full)
             torch.cuda.synchronize()
             assert torch.equal(C_full, ref) and torch.equal(C_local, ref), (m, n, p)
+            # 2-D lifting on a 1 x 1 grid through the fused-gather entry
+            C_full.fill_(float("nan"))
+            C_blk = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+            moa.gemm_lifted_2d(m, p, 1, 1, A, B, C_blk, comm, C_full=C_full)
+            torch.cuda.synchronize()
+            assert torch.equal(C_full, ref) and torch.equal(C_blk, ref), (m, n, p)
             comm.free_window(C_full)
     finally:
         comm.close()
