@@ -366,8 +366,8 @@ int run_plan(const moa_plan_t& plan, const GemmArgs& g, int dtype, cudaStream_t 
 int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t stream) {
   int rc = validate_g(g, dtype);
   if (rc) return rc;
-  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64) {
-    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 only");
+  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
+    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 and MOA_F32 only");
     return MOA_ERR_INVALID_DTYPE;
   }
   DeviceShape ds;
@@ -872,8 +872,8 @@ int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks) {
 static int gemm_reserving(const GemmArgs& g, int dtype, cudaStream_t s, int reserve) {
   int rc = validate_g(g, dtype);
   if (rc) return rc;
-  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64) {
-    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 only");
+  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
+    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 and MOA_F32 only");
     return MOA_ERR_INVALID_DTYPE;
   }
   DeviceShape ds;
@@ -1053,7 +1053,7 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
   // columns of C_full (row stride p) and stored by the same epilogue into every
   // peer's C_full over NVLink; no workspace, no per-rank broadcasts of C.
   const moa_comm_s::Window* win =
-      (C_full && m * p > 0 && dtype == MOA_F64 && comm->nranks - 1 <= kMaxPeerDst) ? find_window(comm, C_full, m * p * es)
+      (C_full && m * p > 0 && (dtype == MOA_F64 || dtype == MOA_F32) && comm->nranks - 1 <= kMaxPeerDst) ? find_window(comm, C_full, m * p * es)
                                                                                   : nullptr;
   if (C_full && m * p > 0 && !win) {
     if ((reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
@@ -1136,8 +1136,8 @@ static int lifted_2d_impl(int64_t m, int64_t n, int64_t p, int grid_rows, int gr
   const int64_t es = elem_size(dtype);
   const moa_comm_s::Window* win = nullptr;
   if (C_full && m * p > 0) {  // the fused gather: C_full must be a symmetric window, fp64
-    if (dtype != MOA_F64) {
-      set_error("moa_gemm_lifted_2d_gather: MOA_F64 only");
+    if (dtype != MOA_F64 && dtype != MOA_F32) {
+      set_error("moa_gemm_lifted_2d_gather: MOA_F64 or MOA_F32 only");
       return MOA_ERR_INVALID_DTYPE;
     }
     if (comm->nranks - 1 > kMaxPeerDst) {
@@ -1223,8 +1223,8 @@ int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda
   GemmArgs g{m, n, p, A, B, C, lda, ldb, ldc, accumulate ? 1 : 0};
   int rc = validate_g(g, dtype);
   if (rc) return rc;
-  if (ndst > 0 && dtype != MOA_F64) {
-    set_error("moa_gemm_scatter: MOA_F64 only");
+  if (ndst > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
+    set_error("moa_gemm_scatter: MOA_F64 or MOA_F32 only");
     return MOA_ERR_INVALID_DTYPE;
   }
   const int64_t es = elem_size(dtype);
@@ -1388,8 +1388,8 @@ int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local,
     set_error("npanels out of range");
     return MOA_ERR_INVALID_SHAPE;
   }
-  if (dtype != MOA_F64) {
-    set_error("moa_gemm_lifted_gather: MOA_F64 only");
+  if (dtype != MOA_F64 && dtype != MOA_F32) {
+    set_error("moa_gemm_lifted_gather: MOA_F64 or MOA_F32 only");
     return MOA_ERR_INVALID_DTYPE;
   }
   if (comm->nranks - 1 > kMaxPeerDst) {

@@ -164,12 +164,14 @@ struct K3Traits {
   static constexpr int kSmem = 1024 + STAGES * kStageBytes + 2 * STAGES * 8;
 };
 
-// ACC is compile-time so the plain path keeps its register allocation.
-template <int STAGES, bool ACC>
+// ACC is compile-time so the plain path keeps its register allocation. PEER: the
+// fused all-gather epilogue (as K1's): every final tile is also stored to each
+// peers.dst[d] (same ldc), e.g. other ranks' C_full over NVLink.
+template <int STAGES, bool ACC, bool PEER>
 __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
     k_sgemm_ffma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int64_t tiles_m,
-                 int64_t tiles_n, int group) {
+                 int64_t tiles_n, int group, const __grid_constant__ PeerDst peers) {
   using Tr = K3Traits<STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -243,6 +245,9 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
       }
     }
     sstore<true>(acc, C, m, p, ldc, tm * Tr::BM, tn * Tr::BN, ty, tx);
+    if constexpr (PEER)
+      for (int d = 0; d < peers.nd; ++d)
+        sstore<true>(acc, reinterpret_cast<float*>(peers.dst[d]), m, p, ldc, tm * Tr::BM, tn * Tr::BN, ty, tx);
   }
 }
 
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
 __global__ void __launch_bounds__(256)
     k_sgemm_generic(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C, int64_t m,
                     int64_t n, int64_t p, int64_t lda, int64_t ldb, int64_t ldc, int accumulate, int64_t tiles_m,
-                    int64_t tiles_n, int group) {
+                    int64_t tiles_n, int group, const __grid_constant__ PeerDst peers) {
   constexpr int BM = 128, BN = 128;
   __shared__ __align__(1024) uint8_t sm[BM * kRowB + kBKf * BN * 4];
   float* sA = reinterpret_cast<float*>(sm);
@@ -285,6 +290,8 @@ __global__ void __launch_bounds__(256)
       ffma_slab(acc, sm, sm + BM * kRowB, ty, tx);
     }
     sstore<false>(acc, C, m, p, ldc, row0, col0, ty, tx);
+    for (int d = 0; d < peers.nd; ++d)  // fused gather epilogue (see K3's PEER)
+      sstore<false>(acc, reinterpret_cast<float*>(peers.dst[d]), m, p, ldc, row0, col0, ty, tx);
   }
 }
 
@@ -300,7 +307,7 @@ void refine_occupancy() {
   std::call_once(once, [] {
     RelaxedCapture relaxed_capture;
     int n = 0;
-    auto kern = k_sgemm_ffma<6, false>;
+    auto kern = k_sgemm_ffma<6, false, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K3Traits<6>::kSmem) == cudaSuccess &&
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, K3Traits<6>::kThreads, K3Traits<6>::kSmem) ==
             cudaSuccess &&
@@ -335,21 +342,26 @@ int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t st
       !encode_2d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.B, n, p, 32, kBKf, CU_TENSOR_MAP_SWIZZLE_128B, g.ldb))
     return MOA_ERR_CUDA;
   float* C = (float*)g.C;
-  auto kern = g.accumulate ? k_sgemm_ffma<6, true> : k_sgemm_ffma<6, false>;
+  const bool peer = g.peers && g.peers->nd > 0;
+  auto kern = g.accumulate ? (peer ? k_sgemm_ffma<6, true, true> : k_sgemm_ffma<6, true, false>)
+                           : (peer ? k_sgemm_ffma<6, false, true> : k_sgemm_ffma<6, false, false>);
+  PeerDst peers{};
+  if (peer) peers = *g.peers;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     RelaxedCapture relaxed_capture;
-    attr_err = cudaFuncSetAttribute(k_sgemm_ffma<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(k_sgemm_ffma<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
+    for (auto k : {k_sgemm_ffma<6, false, false>, k_sgemm_ffma<6, true, false>, k_sgemm_ffma<6, false, true>,
+                   k_sgemm_ffma<6, true, true>})
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::kSmem);
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
   kern<<<plan.grid, Tr::kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                                       plan.raster_group);
+                                                       plan.raster_group, peers);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_ffma launch: ") + cudaGetErrorString(e));
@@ -359,9 +371,11 @@ int launch_sgemm_ffma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t st
 }
 
 int launch_sgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
+  PeerDst peers{};
+  if (g.peers) peers = *g.peers;
   k_sgemm_generic<<<plan.grid, 256, 0, stream>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.m, g.n, g.p,
                                                  g.lda, g.ldb, g.ldc, g.accumulate, plan.tiles_m, plan.tiles_n,
-                                                 plan.raster_group);
+                                                 plan.raster_group, peers);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_generic launch: ") + cudaGetErrorString(e));

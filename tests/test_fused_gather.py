@@ -33,7 +33,7 @@ def test_scatter_validation_without_gpu():
     f = moa._moa_gemm_scatter
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 9, arr, 0, None) == 1            # ndst > 8
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, -1, arr, 0, None) == 1           # ndst < 0
-    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, arr, 1, None) == 2            # fp32 + destinations
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, arr, 2, None) == 2            # 3xTF32 + destinations
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, None, 0, None) == 3           # NULL dst array
     bad = (moa._vp * 2)(D, None)
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 2, bad, 0, None) == 3            # NULL destination
@@ -113,13 +113,32 @@ def test_scatter_accumulate_chain_last_panel(cuda_device):
 
 
 @pytest.mark.gpu
-def test_scatter_rejects_fp32(cuda_device):
+@pytest.mark.parametrize("shape", [(2000, 64, 2048), (300, 200, 260), (257, 33, 131)],
+                         ids=["k3-multiwave", "k3-ragged", "k3-generic"])
+def test_scatter_fp32_exact_bitwise(cuda_device, shape):
+    """K3 / K3g PEER epilogue: fp32 exact (fused fma chain, k ascending) in every
+    destination, bitwise the fp32 fused oracle."""
+    m, n, p = shape
+    A = torch.from_numpy(I.host_matrix(m, n, 3, I.ID_A, dtype=np.float32)).to(cuda_device)
+    B = torch.from_numpy(I.host_matrix(n, p, 3, I.ID_B, dtype=np.float32)).to(cuda_device)
+    ref = O.ip(A.cpu().numpy(), B.cpu().numpy(), fused=True)
+    C = torch.full((m, p), float("nan"), dtype=torch.float32, device=cuda_device)
+    dst = [torch.full((m, p), float("nan"), dtype=torch.float32, device=cuda_device) for _ in range(3)]
+    moa.gemm_scatter(A, B, C, dst)
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy(), ref)
+    for t in dst:
+        assert torch.equal(t, C)
+
+
+@pytest.mark.gpu
+def test_scatter_rejects_3xtf32(cuda_device):
     A = torch.ones((64, 64), dtype=torch.float32, device=cuda_device)
     C = torch.empty((64, 64), dtype=torch.float32, device=cuda_device)
     d = torch.empty((64, 64), dtype=torch.float32, device=cuda_device)
-    with pytest.raises(moa.MoAError) as e:
-        moa.gemm_scatter(A, A, C, [d])
-    assert e.value.name == "MOA_ERR_INVALID_DTYPE"
+    arr = (moa._vp * 1)(d.data_ptr())
+    rc = moa._moa_gemm_scatter(64, 64, 64, A.data_ptr(), 64, A.data_ptr(), 64, C.data_ptr(), 64, 0, 1, arr, 2, None)
+    assert rc == 2  # MOA_ERR_INVALID_DTYPE: the tcgen05 variant has no gather epilogue
 
 
 def _free_port():
@@ -167,10 +186,12 @@ def test_lifted_gather_single_rank_nccl(cuda_device):
         with pytest.raises(moa.MoAError) as e:
             moa.gemm_lifted_gather(64, A, B, plain, comm)
         assert e.value.name == "MOA_ERR_NOT_REGISTERED"
+        # fp32 exact through the same collective path (K3 PEER)
         w = comm.alloc_window((64, 64), torch.float32)
-        with pytest.raises(moa.MoAError) as e:
-            moa.gemm_lifted_gather(64, A.float(), B.float(), w, comm)
-        assert e.value.name == "MOA_ERR_INVALID_DTYPE"
+        w.fill_(float("nan"))
+        moa.gemm_lifted_gather(64, A.float(), B.float(), w, comm)
+        torch.cuda.synchronize()
+        assert torch.equal(w, moa.gemm(A.float(), B.float()))
         with pytest.raises(moa.MoAError) as e:
             comm.window_peer(plain, 0)
         assert e.value.name == "MOA_ERR_NOT_REGISTERED"
