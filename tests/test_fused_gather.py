@@ -61,21 +61,25 @@ def _operands(m, n, p, seed, dev):
     return A, B
 
 
-# (shape, what it exercises)
+# (shape, what it exercises, the chooser's (bm, bn) for it or None)
 _SHAPES = [
-    ((200, 144, 176), "latency tiles 16x32"),
-    ((2000, 48, 2000), "128x128 stream-K only (split tiles)"),
-    ((2600, 160, 2000), "128x128 dynamic tiles + stream-K runs"),
-    ((1000, 256, 300), "ragged tail"),
-    ((257, 33, 131), "generic kernel (odd n, p)"),
-    ((300, 0, 200), "n = 0: zero fill"),
+    ((200, 144, 176), "latency tiles 16x32", (16, 32)),
+    ((1920, 1024, 1920), "128x128 stream-K only (split tiles)", (128, 128)),
+    ((2560, 1024, 2560), "128x128 dynamic tiles + stream-K runs", (128, 128)),
+    ((2000, 48, 2000), "64x32 shallow k, stream-K over 3 CTAs per SM", (64, 32)),
+    ((1000, 256, 300), "ragged tail", None),
+    ((257, 33, 131), "generic kernel (odd n, p)", None),
+    ((300, 0, 200), "n = 0: zero fill", None),
 ]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shape,what", _SHAPES, ids=[w for _, w in _SHAPES])
-def test_scatter_every_destination_bitwise(cuda_device, shape, what):
+@pytest.mark.parametrize("shape,what,tile", _SHAPES, ids=[w for _, w, _ in _SHAPES])
+def test_scatter_every_destination_bitwise(cuda_device, shape, what, tile):
     m, n, p = shape
+    if tile is not None:  # the schedule this case is meant to exercise
+        pl = moa.plan(m, n, p)
+        assert (pl.bm, pl.bn) == tile, (what, pl)
     A, B = _operands(m, n, p, 7, cuda_device)
     ref = O.ip(A.cpu().numpy(), B.cpu().numpy(), fused=True) if n else np.zeros((m, p))
     for nd in (1, 3, 8):
