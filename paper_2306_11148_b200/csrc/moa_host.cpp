@@ -622,7 +622,11 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
     bnd[++P] = m;
   }
   const bool first_chain = chain && P > 1 && bnd[1] < m;
-  const int64_t KB = first_chain ? 8 : 1;
+  // With a communicator the number of B k-panels (= broadcasts) must be the same on
+  // every rank, so it depends only on (n, dtype), never on this rank's row count; a
+  // rank without a row-panel split still chains its single panel over them (bitwise
+  // the same result).
+  const int64_t KB = (comm ? chain : first_chain) ? 8 : 1;
   int64_t kb[kMaxHostPanels + 1];
   for (int64_t j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
   if ((e = cudaEventRecord(hp->ev0, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");

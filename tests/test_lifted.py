@@ -290,10 +290,13 @@ def test_lifted_host_pipeline_single_rank(cuda_device):
         dist.init_process_group("gloo", rank=0, world_size=1)
     comm = moa.Comm(device=0)
     try:
-        for (m, n, p) in [(6400, 640, 384), (300, 200, 100), (1000, 1000, 130)]:
+        # (1000 x 1000: n >= 512 but too few rows for a row-panel split — with a
+        #  communicator it still chains over the 8 B k-panels every rank broadcasts)
+        for (m, n, p) in [(6400, 640, 384), (300, 200, 100), (1000, 1000, 130), (0, 640, 64)]:
             A = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
             B = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
-            I.device_fill(A, 4, I.ID_A)
+            if m:
+                I.device_fill(A, 4, I.ID_A)
             I.device_fill(B, 4, I.ID_B)
             ref = moa.gemm(A, B).cpu()
             hA, hB = A.cpu().pin_memory(), B.cpu().pin_memory()
