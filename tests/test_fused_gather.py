@@ -47,6 +47,10 @@ def test_scatter_validation_without_gpu():
     assert moa._moa_gemm_lifted_gather(4, 4, 4, A, B, C, 0, None, None, 0) == 3
     assert moa._moa_comm_alloc_window(None, 64, moa._vp()) == 3
     assert moa._moa_status_string(10) == b"MOA_ERR_NOT_REGISTERED"
+    assert moa._moa_gemm_lifted_2d_gather(4, 4, 4, 1, 1, A, B, C, D, 0, None, None) == 3
+    assert moa._moa_gemm_lifted_host(4, 4, 4, A, B, C, A, B, C, 0, None, None) == 3
+    assert moa._moa_comm_window_peer(None, A, 0, moa._vp()) == 3
+    assert moa._moa_comm_free_window(None, A) == 3
 
 
 # --------------------------------------------------------------------- GPU ----
