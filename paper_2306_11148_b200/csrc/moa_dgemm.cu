@@ -10,7 +10,11 @@
 //                    register accumulators. Work: dynamically claimed tiles plus
 //                    stream-K runs for the partial last wave, whose cut tiles
 //                    continue the fma chain from the stored partial (bitwise);
-//                    launched with programmatic dependent launch.
+//                    launched with programmatic dependent launch. The PEER
+//                    instantiation also stores every final tile to up to 8
+//                    further destinations (other ranks' C_full over NVLink):
+//                    the all-gather of the row-lifted product fused into the
+//                    epilogue (moa_gemm_lifted_gather / moa_gemm_scatter).
 // K2 k_dgemm_generic: same arithmetic, plain predicated loads (odd n or p,
 //                    pointers not 16-byte aligned — shapes TMA cannot describe).
 //

@@ -9,7 +9,9 @@
 //                     tiles and run packed FFMA2 (fma.rn.f32x2) outer products:
 //                     the scalar A[i][k] (broadcast operand, no MOV) times the
 //                     contiguous pair B[k][j..j+1] — the scalar-vector axpy of
-//                     Fig. 1, two columns per instruction.
+//                     Fig. 1, two columns per instruction. As K1,
+//                     a PEER instantiation fuses the all-gather of C into the
+//                     epilogue.
 // K3g k_sgemm_generic: same arithmetic, predicated loads (n or p not multiples
 //                     of 4, pointers not 16-B aligned).
 //
