@@ -25,20 +25,25 @@ SCRIPT = textwrap.dedent(r'''
     host = [(I.host_matrix(m, n, 7, I.ID_A), I.host_matrix(n, p, 7, I.ID_B)) for (m, n, p) in shapes]
     dev = [(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()) for a, b in host]
     outs = [torch.full((a.shape[0], b.shape[1]), float("nan"), dtype=torch.float64, device="cuda") for a, b in dev]
+    # and the fused-gather epilogue (K1 PEER) into a second block
+    sc = torch.full_like(outs[1], float("nan"))
+    sd = torch.full_like(outs[1], float("nan"))
     s = torch.cuda.Stream()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):   # first library calls of this process
             for (a, b), c in zip(dev, outs):
                 moa.gemm(a, b, out=c)
+            moa.gemm_scatter(dev[1][0], dev[1][1], sc, [sd])
     torch.cuda.synchronize()
     for rep in range(3):
-        for c in outs:
+        for c in outs + [sc, sd]:
             c.fill_(float("nan"))
         g.replay()
         torch.cuda.synchronize()
         for (a, b), c in zip(host, outs):
             assert np.all(c.cpu().numpy() == O.ip(a, b, fused=True)), ("replay", rep, a.shape, b.shape)
+        assert torch.equal(sc, outs[1]) and torch.equal(sd, outs[1]), ("scatter replay", rep)
     print("GRAPH OK")
 ''')
 
