@@ -116,3 +116,38 @@ def test_gemm_acc_validation_without_gpu():
     assert moa._moa_gemm_acc(4, 8, 8, A, 7, B, 8, C, 8, 0, 0, None) == 1      # lda < n
     assert moa._moa_gemm_acc(4, 8, 8, A, 8, B, 8, C, 7, 0, 0, None) == 1      # ldc < p
     assert moa._moa_gemm_acc(4, 8, 8, A, 8, B, 8, A + 8 * 20, 8, 0, 0, None) == 4  # C inside A's span
+
+
+def test_header_is_plain_c_and_links_from_c(tmp_path):
+    """include/moa.h compiles as C99 (no C++ or torch types), and a plain C program
+    links libmoa.so and calls host-only entry points through it."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "abi_user.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include <string.h>
+#include "moa.h"
+int main(void) {
+  int64_t row0 = -1, rows = -1, off = -1, cnt = -1, b = -1;
+  const int64_t shape[2] = {3, 4}, idx[2] = {1, 2};
+  if (moa_abi_version() != MOA_ABI_VERSION) return 1;
+  if (moa_lift_rows(37, 2, 1, &row0, &rows) != MOA_OK || row0 != 19 || rows != 18) return 2;
+  if (moa_psi(2, shape, 2, idx, &off, &cnt) != MOA_OK || off != 6 || cnt != 1) return 3;
+  if (moa_select_block_paper(32 * 1024, 8, &b) != MOA_OK || b != 32) return 4;
+  if (strcmp(moa_status_string(MOA_ERR_ALIASING), "MOA_ERR_ALIASING") != 0) return 5;
+  if (moa_gemm(-1, 2, 2, 0, 0, 0, MOA_F64, 0) != MOA_ERR_INVALID_SHAPE) return 6;
+  printf("C ABI OK\n");
+  return 0;
+}
+""")
+    libdir = os.path.dirname(moa.lib_path)
+    exe = tmp_path / "abi_user"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                        "-o", str(exe), "-L", libdir, "-l:libmoa.so", "-Wl,-rpath," + libdir],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "C ABI OK" in r.stdout, (r.returncode, r.stdout, r.stderr)
