@@ -11,8 +11,12 @@ independent, Fig. 1 / P:99) plus a Freivalds product check.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 from inputs import inputs as I
 from oracle import oracle as O
@@ -325,3 +329,53 @@ def test_strided_output_and_validation(cuda_device):
     assert torch.all(big[:, :2] == -1) and torch.all(big[:, 2 + p:] == -1)
     rc = moa._moa_gemm_acc(m, n, p, tA.data_ptr(), n - 1, tB.data_ptr(), p, big.data_ptr(), p + 10, 0, 0, None)
     assert rc == 1  # lda < n
+
+
+@pytest.mark.gpu
+def test_pure_c_caller_through_the_abi(cuda_device, tmp_path):
+    """The boundary without Python or torch: a C99 program allocates with the CUDA
+    runtime, calls moa_gemm on integer-valued fp64 data (every summation order gives
+    the same bits, pin P6) and compares with its own triple loop exactly."""
+    import shutil
+    import subprocess
+    import paper_2306_11148_b200 as moa
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "c_gemm.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include <stdlib.h>
+#include <cuda_runtime.h>
+#include "moa.h"
+int main(void) {
+  const int64_t m = 300, n = 200, p = 260;
+  double *hA = malloc(sizeof(double) * m * n), *hB = malloc(sizeof(double) * n * p);
+  double *hC = malloc(sizeof(double) * m * p), *dA, *dB, *dC;
+  for (int64_t i = 0; i < m * n; ++i) hA[i] = (double)((i * 7 + 3) % 9) - 4.0;
+  for (int64_t i = 0; i < n * p; ++i) hB[i] = (double)((i * 5 + 1) % 9) - 4.0;
+  if (cudaMalloc((void**)&dA, sizeof(double) * m * n) || cudaMalloc((void**)&dB, sizeof(double) * n * p) ||
+      cudaMalloc((void**)&dC, sizeof(double) * m * p)) return 10;
+  cudaMemcpy(dA, hA, sizeof(double) * m * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, hB, sizeof(double) * n * p, cudaMemcpyHostToDevice);
+  int rc = moa_gemm(m, n, p, dA, dB, dC, MOA_F64, NULL);
+  if (rc != MOA_OK) { printf("moa_gemm: %s %s\n", moa_status_string(rc), moa_last_error()); return 11; }
+  if (cudaDeviceSynchronize() != cudaSuccess) return 12;
+  cudaMemcpy(hC, dC, sizeof(double) * m * p, cudaMemcpyDeviceToHost);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < p; ++j) {
+      double s = 0.0;
+      for (int64_t k = 0; k < n; ++k) s += hA[i * n + k] * hB[k * p + j];
+      if (s != hC[i * p + j]) { printf("mismatch at %ld %ld\n", (long)i, (long)j); return 13; }
+    }
+  printf("C GEMM OK\n");
+  return 0;
+}
+""")
+    libdir = os.path.dirname(moa.lib_path)
+    exe = tmp_path / "c_gemm"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                        str(src), "-o", str(exe), "-L", libdir, "-l:libmoa.so", "-L", "/usr/local/cuda/lib64",
+                        "-lcudart", "-Wl,-rpath," + libdir + ":/usr/local/cuda/lib64"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "C GEMM OK" in r.stdout, (r.returncode, r.stdout, r.stderr)
