@@ -265,9 +265,16 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
       // Latency tiles (16x16 outputs per warp, one resident CTA per tile): only for
       // tiny problems (fewer 64x32 tiles than SMs), where the time is the longest
       // DMMA chain per SM sub-partition: ceil(warps / (4 SMs)) warps of 16x16 each.
-      if ((double)m * (double)p >= (double)ds.sms * 64.0 * 32.0) continue;
+      // For thin p (<= 32 columns: one 16x32 tile spans the row) the 16x32 tiles stay
+      // candidates up to 2x that size at 0.85 of the model: 16384 x {64, 512, 4096} x 32
+      // run 5.7 / 23.3 / 165 us with them vs 9.7 / 28.6 / 180 us with 64x32 stream-K
+      // (profiles/r01_thin_p.jsonl; at 30000 x 128 x 32 64x32 is ahead again).
+      // (Extending the gate to every tile picked 16x16 tiles far too often.)
+      const double mp = (double)m * (double)p, one = (double)ds.sms * 64.0 * 32.0;
+      const bool thin = c.bn == 32 && p <= 32 && mp < 2.0 * one;
+      if (mp >= one && !thin) continue;
       const int64_t warps = tiles * ((int64_t)c.bm * c.bn / 256), smsp = 4LL * ds.sms;
-      eff = (double)m * (double)p / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * eta;
+      eff = mp / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * eta * (mp < one ? 1.0 : 0.85);
     }
     // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
     // cut tiles cost a partial store + reload and an extra pipeline fill: -1%, and
