@@ -167,7 +167,19 @@ int moa_gemm_lifted_host(int64_t m, int64_t n, int64_t p, const void* A_host, co
  *   C_full  : NULL, or a device m x p buffer that receives all of C on every
  *             rank (gather, reading R14).
  * Bitwise identical to moa_gemm on one GPU (row-block invariance of the plan).
- * Errors are detected identically on every rank before any NCCL call.
+ * If B lies inside a window from moa_comm_alloc_window (every rank passes its own
+ * copy), the exchange is copy-engine pulls instead of NCCL broadcasts
+ * (MOA_XF_PULL_B in moa_exchange_plan): after an entry barrier every rank g > 0
+ * reads B's k-panels (moa_pull_panels) from rank 0's copy over NVLink into its
+ * own, on a side stream, and the compute of panel j waits only for panel j; no SM
+ * is taken from the GEMM. Rank 0 computes its rows in one launch. An exit barrier
+ * keeps rank 0's B unchanged until every pull is complete.
+ * Errors: checks that depend only on (m, n, p, dtype, G, npanels) fail identically
+ * on every rank before any collective. Checks of THIS rank's pointers (NULL,
+ * alignment, overlap) can fail on one rank only; that rank returns before any
+ * collective while its peers block in the first one — as with NCCL, any error
+ * from a collective call is fatal for the communicator (destroy it on every rank).
+ * moa_comm_agree lets a caller make the local checks collective first.
  * ------------------------------------------------------------------------ */
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                     int dtype, void* stream, moa_comm_t comm);
@@ -244,8 +256,10 @@ int moa_gemm_lifted_2d_gather(int64_t m, int64_t n, int64_t p, int grid_rows, in
  * moa_comm_window_peer). Every destination receives exactly the bits of C. With
  * accumulate != 0 (the last k-panel of a chain) only C is read. MOA_F64 or
  * MOA_F32 (the exact kernels; MOA_ERR_INVALID_DTYPE otherwise); 0 <= ndst <= 8 (MOA_ERR_INVALID_SHAPE); destinations
- * non-NULL when m*p > 0, aligned to 8 bytes, and disjoint from A, B, C and each
- * other (MOA_ERR_ALIASING). Asynchronous on `stream`. */
+ * non-NULL when m*p > 0, aligned to the element size (MOA_ERR_MISALIGNED otherwise),
+ * and disjoint from A, B, C and each other (MOA_ERR_ALIASING). A destination that is
+ * not 16-byte aligned routes the call to the generic kernel (same bits; the TMA
+ * kernels' epilogue uses 16-byte stores). Asynchronous on `stream`. */
 int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, const void* B, int64_t ldb,
                      void* C, int64_t ldc, int accumulate, int ndst, void* const* dst, int dtype, void* stream);
 
@@ -280,6 +294,57 @@ int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local,
  * not travel (nranks == 1), else ceil(bytes(B) / 512 MiB) clamped to [1, 8] and
  * to n/64. Pure function. */
 int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks);
+
+/* ------------------------------------------------------------------------
+ * The exchange plan of the lifted paths (row a7 of the build; P:147-148, P:165,
+ * P:188): the static, ordered list of collectives a lifted call issues on each
+ * rank. It is a pure function of (variant, m, n, p, dtype, G, rank, grid, npanels,
+ * flags) — the executors of moa_gemm_lifted*, _cols, _2d and _host walk exactly this
+ * list — so ranks issue identical sequences (per communicator) by construction,
+ * and the bytes each call moves can be checked against the model without a GPU.
+ *   op      : MOA_COLL_BROADCAST (NCCL, in place unless noted), MOA_COLL_ALLGATHER
+ *             (NCCL), MOA_COLL_BARRIER (one-int NCCL all-reduce on the stream),
+ *             MOA_COLL_PULL (copy-engine read of `count` elements of rank `root`'s
+ *             symmetric window over NVLink into this rank's copy; no SMs, no NCCL);
+ *   comm    : which communicator carries it (world, the CTA-limited pipe split,
+ *             the 2-D row / column splits);
+ *   root    : broadcast root / pull source, as a rank of `comm`; -1 otherwise;
+ *   group   : ops with the same group id > 0 are issued in one ncclGroupStart/End;
+ *   operand : what travels (MOA_OPERAND_A, _B, _C);
+ *   phase   : 0 before the compute, 1 overlapped with it (k-panels of B: the
+ *             compute of panel `panel` waits for this op), 2 after it;
+ *   offset, count : the data's element offset in the destination operand, and its
+ *             element count (all-gather: each rank's send count).
+ * Ops on a 1-rank communicator are never issued, so G == 1 plans are empty. */
+typedef enum { MOA_COLL_BROADCAST = 1, MOA_COLL_ALLGATHER = 2, MOA_COLL_BARRIER = 3, MOA_COLL_PULL = 4 } moa_coll_op;
+typedef enum { MOA_COMM_WORLD = 0, MOA_COMM_PIPE = 1, MOA_COMM_ROW = 2, MOA_COMM_COL = 3 } moa_comm_kind;
+typedef enum { MOA_OPERAND_A = 0, MOA_OPERAND_B = 1, MOA_OPERAND_C = 2 } moa_operand;
+typedef enum {
+  MOA_XPLAN_ROWS = 0,      /* moa_gemm_lifted_ex / moa_gemm_lifted_gather */
+  MOA_XPLAN_ROWS_HOST = 1, /* moa_gemm_lifted_host */
+  MOA_XPLAN_COLS = 2,      /* moa_gemm_lifted_cols */
+  MOA_XPLAN_2D = 3         /* moa_gemm_lifted_2d / _2d_gather */
+} moa_xplan_variant;
+#define MOA_XF_GATHER 1       /* C_full given, gathered with NCCL (rows: all-gather / per-rank broadcasts; cols: via workspace) */
+#define MOA_XF_FUSED_GATHER 2 /* C_full inside a window: gather fused into the GEMM epilogue, entry/exit barriers */
+#define MOA_XF_PULL_B 4       /* rows: B inside a window on every rank: copy-engine pulls of B's k-panels from rank 0 */
+typedef struct {
+  int32_t op, comm, root, group, operand, phase, panel, reserved;
+  int64_t offset, count;
+} moa_coll_t;
+
+/* Fills ops[0..*nops) (at most max_ops; MOA_ERR_INVALID_SHAPE if more are needed,
+ * with *nops = the number needed). grid_rows/grid_cols are used by MOA_XPLAN_2D only;
+ * npanels as moa_gemm_lifted_ex (0 = static choice). Pure function (no device). */
+int moa_exchange_plan(int variant, int64_t m, int64_t n, int64_t p, int dtype, int nranks, int rank, int grid_rows,
+                      int grid_cols, int npanels, int flags, moa_coll_t* ops, int max_ops, int* nops);
+
+/* moa_pull_panels — the static k-panel split of B for MOA_XF_PULL_B: the first panel is
+ * small (n/64 rows, a multiple of 32, at least 32) so that little of the pull is
+ * exposed before the first panel's compute, and each later panel doubles (its pull
+ * hides behind the previous panel's compute), at most 16 panels. Writes the panel
+ * boundaries bnd[0..K] (bnd[0] = 0, bnd[K] = n) when bnd != NULL; returns K (>= 1). */
+int moa_pull_panels(int64_t n, int64_t* bnd);
 
 /* ------------------------------------------------------------------------
  * moa_psi — MoA psi on a row-major array (appendix; bracket bridge
@@ -332,6 +397,12 @@ int moa_kron(int64_t m, int64_t n, int64_t p, int64_t q, const void* A, const vo
 int moa_comm_get_unique_id(unsigned char id[128]);
 int moa_comm_init(int nranks, int rank, const unsigned char id[128], int device, moa_comm_t* comm);
 int moa_comm_destroy(moa_comm_t comm);
+
+/* moa_comm_agree — COLLECTIVE, SYNCHRONOUS: *global_status = the maximum over ranks of
+ * local_status (e.g. this rank's result of validating its arguments), via a one-int
+ * NCCL all-reduce on the communicator's side stream, which this call synchronises.
+ * Lets every rank fail together before entering a lifted call. */
+int moa_comm_agree(moa_comm_t comm, int local_status, int* global_status);
 
 const char* moa_status_string(int status);
 const char* moa_last_error(void);

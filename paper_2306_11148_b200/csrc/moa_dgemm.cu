@@ -526,7 +526,7 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   unsigned int *flags = nullptr, *ctr = nullptr;
   if (plan.tiles > plan.grid) {
     const bool sk = use_stream_k(plan.tiles, plan.grid);
-    if (sk && !acquire_split_flags((unsigned)plan.grid + 1, &flags)) return MOA_ERR_CUDA;
+    if (sk && !acquire_split_flags((unsigned)plan.grid + 1, stream, &flags)) return MOA_ERR_CUDA;
     // no counter when every tile is a stream-K run (tiles < 2G: run = CTA index)
     if (!(sk && sk_first_tile(plan.tiles, plan.grid) == 0) && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   }

@@ -47,7 +47,7 @@ struct moa_comm_s {
     std::vector<void*> peer;  // peer[r] = rank r's copy
   };
   std::vector<Window> windows;
-  int* barrier_buf = nullptr;  // one int, the operand of the barrier all-reduce
+  int* barrier_buf = nullptr;  // two ints: [0] the barrier all-reduce's operand, [1] moa_comm_agree's
 };
 
 namespace moa {
@@ -205,11 +205,17 @@ int validate(int64_t m, int64_t n, int64_t p, const void* A, const void* B, cons
 
 // Is this call describable by the TMA kernels? (row strides multiple of 16 B,
 // bases 16-B aligned, coordinates fit the tensor map's int32.)
+// The extra C destinations of the fused-gather epilogue are written with the same
+// 16-byte vector stores as C (K1 double2, K3 float4), so they must be 16-B aligned
+// too; an 8-B-aligned fp64 destination routes the call to the generic kernels, which
+// store one element at a time (same bits).
 bool tma_eligible(const GemmArgs& g, int es) {
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   const int per16 = 16 / es;
-  return (g.lda % per16 == 0) && (g.ldb % per16 == 0) && (g.ldc % per16 == 0) && (g.p % per16 == 0) &&
-         al16(g.A) && al16(g.B) && al16(g.C) && g.m < INT32_MAX && g.n < INT32_MAX && g.p < INT32_MAX;
+  bool ok = (g.lda % per16 == 0) && (g.ldb % per16 == 0) && (g.ldc % per16 == 0) && (g.p % per16 == 0) && al16(g.A) &&
+            al16(g.B) && al16(g.C) && g.m < INT32_MAX && g.n < INT32_MAX && g.p < INT32_MAX;
+  for (int d = 0; ok && g.peers && d < g.peers->nd; ++d) ok = al16(g.peers->dst[d]);
+  return ok;
 }
 
 // Persistent grid. K1 (stream-K runs, moa_ptx.cuh sk_run) needs grid <= tiles and all
@@ -562,6 +568,12 @@ int moa_gemm_acc(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda, co
 
 static int gemm_reserving(const GemmArgs& g, int dtype, cudaStream_t s, int reserve);
 static int pipe_comm(moa_comm_t comm, ncclComm_t* out);
+static int issue_nccl(moa_comm_t comm, const moa_coll_t& o, void* data, const void* send, int dtype, cudaStream_t s);
+namespace {
+int host_panel_bounds(int64_t n, int dtype, bool comm, bool first_chain, int64_t* kb);
+std::vector<moa_coll_t> plan_vec(int variant, int64_t m, int64_t n, int64_t p, int dtype, int G, int rank, int gr,
+                                 int gc, int npanels, int flags);
+}  // namespace
 
 // The end-to-end pipeline of moa_gemm_host; with a communicator, the rank's rows
 // of the row-lifted product (moa_gemm_lifted_host): B's k-panels cross the host
@@ -632,10 +644,12 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
   // With a communicator the number of B k-panels (= broadcasts) must be the same on
   // every rank, so it depends only on (n, dtype), never on this rank's row count; a
   // rank without a row-panel split still chains its single panel over them (bitwise
-  // the same result).
-  const int64_t KB = (comm ? chain : first_chain) ? 8 : 1;
-  int64_t kb[kMaxHostPanels + 1];
-  for (int64_t j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
+  // the same result). The broadcasts are the exchange plan's (MOA_XPLAN_ROWS_HOST).
+  int64_t kb[kMaxPanels + 1];
+  const int64_t KB = host_panel_bounds(n, dtype, comm != nullptr, first_chain, kb);
+  const std::vector<moa_coll_t> xops =
+      comm ? plan_vec(MOA_XPLAN_ROWS_HOST, m, n, p, dtype, comm->nranks, comm->rank, 0, 0, 0, 0)
+           : std::vector<moa_coll_t>();
   if ((e = cudaEventRecord(hp->ev0, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   if ((e = cudaStreamWaitEvent(hp->h2d, hp->ev0, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
   if ((e = cudaStreamWaitEvent(hp->d2h, hp->ev0, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
@@ -653,8 +667,7 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
   // with a communicator after its broadcast from rank 0 (every processor
   // reads all of B), issued in the same order on every rank
   cudaEvent_t* evB = comm ? comm->ev_panel : hp->evB;
-  ncclComm_t pipe = nullptr;  // panels after the first overlap GEMMs: CTA-limited comm
-  if (comm && KB > 1 && (rc = pipe_comm(comm, &pipe))) return rc;
+  bool pipe_used = false;  // NCCL panels in flight on the CTA-limited comm: leave SMs free
   for (int64_t j = 0; j < KB; ++j) {
     if (b_root) {
       if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
@@ -663,12 +676,11 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
     if (comm) {
       if (b_root && (e = cudaStreamWaitEvent(comm->side, hp->evB[j], 0)) != cudaSuccess)
         return cuda_fail(e, "cudaStreamWaitEvent");
-      if (kb[j + 1] > kb[j]) {
-        char* bp = (char*)B_dev + kb[j] * p * es;
-        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((kb[j + 1] - kb[j]) * p), nccl_type(dtype), 0,
-                                       j == 0 ? comm->nccl : pipe, comm->side);
-        if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B panel)");
-      }
+      for (const auto& o : xops)
+        if (o.panel == j) {
+          if ((rc = issue_nccl(comm, o, B_dev, nullptr, dtype, comm->side))) return rc;
+          pipe_used = pipe_used || o.comm == MOA_COMM_PIPE;
+        }
       if ((e = cudaEventRecord(comm->ev_panel[j], comm->side)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     }
   }
@@ -689,7 +701,7 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
         const GemmArgs g{rows, kb[j + 1] - kb[j], p, (const char*)A_dev + (r0 * n + kb[j]) * es, (const char*)B_dev + kb[j] * p * es,
                          (char*)C_dev + r0 * p * es, n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
         // with a communicator, later B panels are still being broadcast: leave SMs free
-        if ((rc = gemm_reserving(g, dtype, s, comm && j < KB - 1 ? kPipeCTAs : 0))) return rc;
+        if ((rc = gemm_reserving(g, dtype, s, pipe_used && j < KB - 1 ? kPipeCTAs : 0))) return rc;
       }
     } else if ((rc = moa_gemm(rows, n, p, (const char*)A_dev + r0 * n * es, B_dev, (char*)C_dev + r0 * p * es, dtype,
                               stream))) {
@@ -775,6 +787,12 @@ int moa_comm_init(int nranks, int rank, const unsigned char id[128], int device,
       delete c;
       return cuda_fail(e, "panel events");
     }
+  if ((e = cudaMalloc(&c->barrier_buf, 2 * sizeof(int))) != cudaSuccess ||
+      (e = cudaMemset(c->barrier_buf, 0, 2 * sizeof(int))) != cudaSuccess) {
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return cuda_fail(e, "barrier buffer");
+  }
   *comm = c;
   return MOA_OK;
 }
@@ -872,6 +890,33 @@ int moa_lift_panels(int64_t n, int64_t p, int dtype, int nranks) {
   return k < 1 ? 1 : (int)k;
 }
 
+int moa_pull_panels(int64_t n, int64_t* bnd) {
+  // A small first panel (little exposed before compute starts), then doubling: the
+  // pull of panel j+1 (twice panel j's rows) overlaps panel j's compute, which at the
+  // configs[4] shapes runs ~1.4x longer than the pull. Boundaries are
+  // multiples of 32 rows of B (TMA alignment of the A column slice).
+  if (n < 64) {
+    if (bnd) {
+      bnd[0] = 0;
+      bnd[1] = n > 0 ? n : 0;
+    }
+    return 1;
+  }
+  int64_t first = (n / 64) / 32 * 32;
+  if (first < 32) first = 32;
+  int K = 0;
+  int64_t b = 0;
+  if (bnd) bnd[0] = 0;
+  while (b < n) {
+    int64_t next = K == 0 ? first : 2 * b;
+    if (next >= n || K == kMaxPanels - 1) next = n;
+    b = next;
+    ++K;
+    if (bnd) bnd[K] = b;
+  }
+  return K;
+}
+
 // A GEMM that leaves `reserve` SMs free for a concurrent collective. A persistent
 // K1 grid takes every SM's registers and shared memory (one 384-thread CTA with
 // 168..232 registers per thread and ~193 KiB of smem), so an NCCL kernel launched
@@ -913,70 +958,349 @@ static int pipe_comm(moa_comm_t comm, ncclComm_t* out) {
   return MOA_OK;
 }
 
-// Steps (1)-(2) of the row-lifted GEMM, shared by moa_gemm_lifted_ex and
-// moa_gemm_lifted_gather: the broadcast of B (optionally pipelined in k-panels) and
-// this rank's rows of C. `last_peers` (fused gather) goes to the launch that writes
-// the FINAL C, i.e. the last k-panel.
-static int lifted_bcast_compute(int64_t n, int64_t p, int64_t rows, const void* A_local, void* B, void* C_local,
-                                int dtype, cudaStream_t s, moa_comm_t comm, int npanels, const PeerDst* last_peers) {
+// ----------------------------- the exchange plan (row a7) -----------------------------
+
+namespace {
+
+// k-panel boundaries of the NCCL-pipelined exchange: multiples of 32 rows of B (TMA
+// alignment of the A column slice), as equal as possible. Each panel of B is ONE
+// contiguous byte range (rows k0..k1 of a row-major B — MoA order). Returns K.
+int nccl_panel_bounds(int64_t n, int K, int64_t* bnd) {
+  if (K < 1) K = 1;
+  if (K > kMaxPanels) K = kMaxPanels;
+  if (n < K) K = n > 0 ? (int)n : 1;
+  for (int j = 0; j <= K; ++j) bnd[j] = j == K ? n : (n * j / K) / 32 * 32;
+  return K;
+}
+
+// Panel boundaries of moa_gemm_lifted_host's B chain (static: 8 k-panels when the
+// first row panel is chained over B, see gemm_host_impl).
+int host_panel_bounds(int64_t n, int dtype, bool comm, bool first_chain, int64_t* kb) {
+  const bool chain = n >= 512 && dtype != MOA_F32_3XTF32;
+  const int KB = (comm ? chain : first_chain) ? 8 : 1;
+  for (int j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
+  return KB;
+}
+
+struct PlanOut {
+  moa_coll_t* ops;
+  int max_ops;
+  int n = 0;
+  void add(int op, int comm, int root, int group, int operand, int phase, int panel, int64_t offset, int64_t count) {
+    if (n < max_ops) {
+      moa_coll_t& o = ops[n];
+      o.op = op;
+      o.comm = comm;
+      o.root = root;
+      o.group = group;
+      o.operand = operand;
+      o.phase = phase;
+      o.panel = panel;
+      o.reserved = 0;
+      o.offset = offset;
+      o.count = count;
+    }
+    ++n;
+  }
+};
+
+// The plan itself. Arguments are validated by the caller (moa_exchange_plan or an
+// executor); every branch depends only on the arguments, never on pointers.
+void build_plan(int variant, int64_t m, int64_t n, int64_t p, int dtype, int G, int rank, int grid_rows,
+                int grid_cols, int npanels, int flags, PlanOut* out) {
+  if (G <= 1) return;  // nothing travels on a 1-rank communicator
+  const bool fused = flags & MOA_XF_FUSED_GATHER, gather = (flags & MOA_XF_GATHER) && !fused,
+             pull = flags & MOA_XF_PULL_B;
+  int64_t bnd[kMaxPanels + 1];
+  switch (variant) {
+    case MOA_XPLAN_ROWS: {
+      if (m * p == 0 && n * p == 0) return;
+      // entry barrier: (fused) no rank stores into a peer's C_full before the peer
+      // reached this call; (pull) rank 0's B is final before anyone reads it
+      if (fused || pull) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 0, -1, 0, 1);
+      if (n * p > 0) {
+        if (pull) {
+          // every processor reads all of B: ranks g > 0 pull it from rank 0
+          if (rank != 0) {
+            const int K = moa_pull_panels(n, bnd);
+            for (int j = 0; j < K; ++j)
+              out->add(MOA_COLL_PULL, MOA_COMM_WORLD, 0, 0, MOA_OPERAND_B, 1, j, bnd[j] * p, (bnd[j + 1] - bnd[j]) * p);
+          }
+        } else {
+          const int K = nccl_panel_bounds(n, npanels > 0 ? npanels : moa_lift_panels(n, p, dtype, G), bnd);
+          for (int j = 0; j < K; ++j)
+            if (bnd[j + 1] > bnd[j] || K == 1)
+              out->add(MOA_COLL_BROADCAST, j == 0 ? MOA_COMM_WORLD : MOA_COMM_PIPE, 0, 0, MOA_OPERAND_B, 1, j,
+                       bnd[j] * p, (bnd[j + 1] - bnd[j]) * p);
+        }
+      }
+      if (gather && m * p > 0) {
+        if (m % G == 0) {
+          out->add(MOA_COLL_ALLGATHER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 2, -1, 0, (m / G) * p);
+        } else {
+          for (int g = 0; g < G; ++g) {
+            int64_t r0, rg;
+            moa_lift_rows(m, G, g, &r0, &rg);
+            if (rg > 0) out->add(MOA_COLL_BROADCAST, MOA_COMM_WORLD, g, 1, MOA_OPERAND_C, 2, -1, r0 * p, rg * p);
+          }
+        }
+      }
+      // exit barrier: (fused) every peer store is complete; (pull) every pull of
+      // rank 0's B is complete before rank 0 may change it
+      if (fused || pull) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 2, -1, 0, 1);
+      return;
+    }
+    case MOA_XPLAN_ROWS_HOST: {
+      int64_t kb[kMaxPanels + 1];
+      const int KB = host_panel_bounds(n, dtype, true, false, kb);
+      for (int j = 0; j < KB; ++j)
+        if (kb[j + 1] > kb[j])
+          out->add(MOA_COLL_BROADCAST, j == 0 ? MOA_COMM_WORLD : MOA_COMM_PIPE, 0, 0, MOA_OPERAND_B, 1, j, kb[j] * p,
+                   (kb[j + 1] - kb[j]) * p);
+      return;
+    }
+    case MOA_XPLAN_COLS: {
+      if (fused) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 0, -1, 0, 1);
+      // every processor needs all of A (ip_cols.c reads A[(i*shr0)+sigma] with no
+      // column-group index): ONE in-place broadcast from rank 0
+      if (m * n > 0) out->add(MOA_COLL_BROADCAST, MOA_COMM_WORLD, 0, 0, MOA_OPERAND_A, 0, -1, 0, m * n);
+      if (fused) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 2, -1, 0, 1);
+      if (gather && m * p > 0)
+        for (int g = 0; g < G; ++g) {  // rank g's column block travels through the workspace
+          int64_t c0, cg;
+          moa_lift_rows(p, G, g, &c0, &cg);
+          if (cg > 0) out->add(MOA_COLL_BROADCAST, MOA_COMM_WORLD, g, 0, MOA_OPERAND_C, 2, -1, c0, m * cg);
+        }
+      return;
+    }
+    case MOA_XPLAN_2D: {
+      const int r = rank / grid_cols, c = rank % grid_cols;
+      int64_t row0, rows, col0, cols;
+      moa_lift_rows(m, grid_rows, r, &row0, &rows);
+      moa_lift_rows(p, grid_cols, c, &col0, &cols);
+      if (fused) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 0, -1, 0, 1);
+      // A's row panel along the process row (root: column 0), B's column panel along
+      // the process column (root: row 0): Figs. 4 and 5 together
+      if (grid_cols > 1 && rows * n > 0) out->add(MOA_COLL_BROADCAST, MOA_COMM_ROW, 0, 0, MOA_OPERAND_A, 0, -1, 0, rows * n);
+      if (grid_rows > 1 && n * cols > 0) out->add(MOA_COLL_BROADCAST, MOA_COMM_COL, 0, 0, MOA_OPERAND_B, 0, -1, 0, n * cols);
+      if (fused) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 2, -1, 0, 1);
+      return;
+    }
+    default: return;
+  }
+}
+
+std::vector<moa_coll_t> plan_vec(int variant, int64_t m, int64_t n, int64_t p, int dtype, int G, int rank, int gr,
+                                 int gc, int npanels, int flags) {
+  PlanOut cnt{nullptr, 0};
+  build_plan(variant, m, n, p, dtype, G, rank, gr, gc, npanels, flags, &cnt);
+  std::vector<moa_coll_t> v((size_t)cnt.n);
+  PlanOut out{v.data(), cnt.n};
+  build_plan(variant, m, n, p, dtype, G, rank, gr, gc, npanels, flags, &out);
+  return v;
+}
+
+}  // namespace
+
+int moa_exchange_plan(int variant, int64_t m, int64_t n, int64_t p, int dtype, int nranks, int rank, int grid_rows,
+                      int grid_cols, int npanels, int flags, moa_coll_t* ops, int max_ops, int* nops) {
+  if (!nops || (max_ops > 0 && !ops)) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (variant < MOA_XPLAN_ROWS || variant > MOA_XPLAN_2D || m < 0 || n < 0 || p < 0 || nranks <= 0 || rank < 0 ||
+      rank >= nranks || npanels < 0 || npanels > kMaxPanels || max_ops < 0 ||
+      (variant == MOA_XPLAN_2D && (grid_rows <= 0 || grid_cols <= 0 || grid_rows * grid_cols != nranks))) {
+    set_error("bad exchange-plan arguments");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  if (elem_size(dtype) == 0) {
+    set_error("unknown dtype");
+    return MOA_ERR_INVALID_DTYPE;
+  }
+  int64_t t;
+  if (!mul_ok(m, n, &t) || !mul_ok(n, p, &t) || !mul_ok(m, p, &t)) {
+    set_error("extent product overflows int64");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  PlanOut out{ops, max_ops};
+  build_plan(variant, m, n, p, dtype, nranks, rank, grid_rows, grid_cols, npanels, flags, &out);
+  *nops = out.n;
+  if (out.n > max_ops) {
+    set_error("ops array too small");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  return MOA_OK;
+}
+
+// ---------------------------------- executors ----------------------------------
+
+static const moa_comm_s::Window* find_window(moa_comm_t comm, const void* ptr, int64_t bytes);
+
+// Barrier of the fused gather / pulled exchange: a one-element all-reduce on the
+// stream. When it completes on rank r, every rank has finished the work it enqueued
+// before it (for the exit barrier: its GEMM, whose peer stores are complete at
+// kernel end, and its pulls, which its last GEMM waited for).
+static int stream_barrier(moa_comm_t comm, cudaStream_t s) {
+  if (comm->nranks <= 1) return MOA_OK;
+  ncclResult_t r = ncclAllReduce(comm->barrier_buf, comm->barrier_buf, 1, ncclInt32, ncclMax, comm->nccl, s);
+  return r == ncclSuccess ? MOA_OK : nccl_fail(r, "ncclAllReduce(barrier)");
+}
+
+static int split_2d(moa_comm_t comm, int grid_rows, int grid_cols) {
+  if (comm->grid_rows == grid_rows && comm->grid_cols == grid_cols) return MOA_OK;
+  const int r = comm->rank / grid_cols, c = comm->rank % grid_cols;
+  if (comm->row_comm) ncclCommDestroy(comm->row_comm);
+  if (comm->col_comm) ncclCommDestroy(comm->col_comm);
+  comm->row_comm = comm->col_comm = nullptr;
+  comm->grid_rows = comm->grid_cols = 0;
+  ncclResult_t q = ncclCommSplit(comm->nccl, r, c, &comm->row_comm, nullptr);
+  if (q == ncclSuccess) q = ncclCommSplit(comm->nccl, c, r, &comm->col_comm, nullptr);
+  if (q != ncclSuccess) return nccl_fail(q, "ncclCommSplit(2-D grid)");
+  comm->grid_rows = grid_rows;
+  comm->grid_cols = grid_cols;
+  return MOA_OK;
+}
+
+static int comm_of(moa_comm_t comm, int kind, ncclComm_t* out) {
+  switch (kind) {
+    case MOA_COMM_WORLD: *out = comm->nccl; return MOA_OK;
+    case MOA_COMM_PIPE: return pipe_comm(comm, out);
+    case MOA_COMM_ROW: *out = comm->row_comm; break;
+    case MOA_COMM_COL: *out = comm->col_comm; break;
+    default: *out = nullptr;
+  }
+  if (!*out) {
+    set_error("sub-communicator missing for an exchange op");
+    return MOA_ERR_NCCL;
+  }
+  return MOA_OK;
+}
+
+// Issue one NCCL op of a plan on stream s. `data` is the destination operand (the
+// op's offset applies to it); `send` (broadcast roots only, may be NULL) is where a
+// root's data comes from when it is not in place.
+static int issue_nccl(moa_comm_t comm, const moa_coll_t& o, void* data, const void* send, int dtype, cudaStream_t s) {
   const int64_t es = elem_size(dtype);
   const ncclDataType_t ty = nccl_type(dtype);
+  if (o.op == MOA_COLL_BARRIER) return stream_barrier(comm, s);
+  ncclComm_t nc;
+  int rc = comm_of(comm, o.comm, &nc);
+  if (rc) return rc;
+  char* dst = (char*)data + o.offset * es;
+  ncclResult_t r;
+  if (o.op == MOA_COLL_BROADCAST)
+    r = ncclBroadcast(send ? send : dst, dst, (size_t)o.count, ty, o.root, nc, s);
+  else if (o.op == MOA_COLL_ALLGATHER)
+    r = ncclAllGather(send, dst, (size_t)o.count, ty, nc, s);
+  else {
+    set_error("not an NCCL op");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  return r == ncclSuccess ? MOA_OK : nccl_fail(r, o.op == MOA_COLL_BROADCAST ? "ncclBroadcast" : "ncclAllGather");
+}
+
+// Row lifting: the plan's collectives around this rank's compute (Fig. 4 ip_rows.c,
+// k = rank), shared by moa_gemm_lifted_ex and moa_gemm_lifted_gather. `last_peers`
+// (fused gather) goes to the launch that writes the FINAL C, i.e. the last k-panel.
+static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const void* A_local, void* B,
+                            void* C_local, void* C_full, int dtype, cudaStream_t s, moa_comm_t comm, int npanels,
+                            int flags, const PeerDst* last_peers) {
+  const int64_t es = elem_size(dtype);
+  const int G = comm->nranks;
+  const bool pull = flags & MOA_XF_PULL_B;
+  const std::vector<moa_coll_t> ops =
+      plan_vec(MOA_XPLAN_ROWS, m, n, p, dtype, G, comm->rank, 0, 0, npanels, flags);
+  // compute panels: the same boundaries as the plan's B ops (or one panel where no B
+  // arrives: rank 0 of a pulled exchange computes its rows in one launch)
+  int64_t bnd[kMaxPanels + 1];
+  int K;
+  if (pull)
+    K = (G > 1 && comm->rank != 0) ? moa_pull_panels(n, bnd) : (bnd[0] = 0, bnd[1] = n, 1);
+  else
+    K = nccl_panel_bounds(n, npanels > 0 ? npanels : moa_lift_panels(n, p, dtype, G), bnd);
+  const moa_comm_s::Window* bwin = pull ? find_window(comm, B, n * p * es) : nullptr;
+  if (pull && n * p > 0 && !bwin) {
+    set_error("MOA_XF_PULL_B without B in a window");
+    return MOA_ERR_NOT_REGISTERED;
+  }
   cudaError_t e;
   int rc;
-  int K = npanels > 0 ? npanels : moa_lift_panels(n, p, dtype, comm->nranks);
-  if (n < K) K = n > 0 ? (int)n : 1;
-  // k-panel boundaries: multiples of 32 rows of B (TMA alignment of the A column
-  // slice), as equal as possible. Each panel of B is ONE contiguous byte range
-  // (rows k0..k1 of a row-major B — MoA order), so it is broadcast as is.
-  int64_t bnd[kMaxPanels + 1];
-  for (int j = 0; j <= K; ++j) {
-    int64_t b = (n * j / K) / 32 * 32;
-    bnd[j] = j == K ? n : b;
-  }
-  if (K == 1) {
-    // (1) every processor needs all of B (ip_rows.c reads B[(sigma*sizer)+j] with no
-    //     processor index): in-place broadcast from rank 0 over NVLink.
-    if (n * p > 0 && comm->nranks > 1) {
-      ncclResult_t r = ncclBroadcast(B, B, (size_t)(n * p), ty, 0, comm->nccl, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B)");
-    }
-  } else {
-    // Pipelined exchange (NEXT-1 step 1): broadcast the k-panels of B on the side
-    // stream, each followed by an event the compute stream waits on. Panel 0 goes
-    // first on the full communicator (nothing computes yet); the later panels go on
-    // the CTA-limited pipe communicator while the panel GEMMs leave kPipeCTAs SMs
-    // free for them (gemm_reserving). With one rank the broadcasts are no-ops but
-    // run the same path.
-    ncclComm_t pipe = nullptr;
-    if ((rc = pipe_comm(comm, &pipe))) return rc;
+  // phase 0: entry barrier
+  for (const auto& o : ops)
+    if (o.phase == 0 && (rc = issue_nccl(comm, o, nullptr, nullptr, dtype, s))) return rc;
+  // phase 1: B's k-panels, on the side stream (when compute overlaps them) with one
+  // event per panel, else on the compute stream
+  bool has[kMaxPanels] = {};
+  bool reserve_sms = false;  // NCCL panel broadcasts in flight need SMs of their own
+  const bool side = K > 1;
+  if (side) {
     if ((e = cudaEventRecord(comm->ev_start, s)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-    if ((e = cudaStreamWaitEvent(comm->side, comm->ev_start, 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
-    for (int j = 0; j < K; ++j) {
-      const int64_t k0 = bnd[j], k1 = bnd[j + 1];
-      if (k1 > k0) {
-        char* bp = (char*)B + k0 * p * es;
-        ncclResult_t r = ncclBroadcast(bp, bp, (size_t)((k1 - k0) * p), ty, 0, j == 0 ? comm->nccl : pipe, comm->side);
-        if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(B panel)");
-      }
-      if ((e = cudaEventRecord(comm->ev_panel[j], comm->side)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(comm->side, comm->ev_start, 0)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamWaitEvent");
+  }
+  for (const auto& o : ops) {
+    if (o.phase != 1) continue;
+    cudaStream_t os = side ? comm->side : s;
+    if (o.op == MOA_COLL_PULL) {
+      // copy-engine read of rank 0's copy over NVLink: no SMs, no NCCL kernel
+      const uintptr_t off = (uintptr_t)B - (uintptr_t)bwin->ptr + (uintptr_t)(o.offset * es);
+      e = cudaMemcpyAsync((char*)B + o.offset * es, (const char*)bwin->peer[(size_t)o.root] + off,
+                          (size_t)(o.count * es), cudaMemcpyDeviceToDevice, os);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(pull B panel)");
+    } else {
+      if ((rc = issue_nccl(comm, o, B, nullptr, dtype, os))) return rc;
+      if (o.comm == MOA_COMM_PIPE) reserve_sms = true;
+    }
+    if (side && o.panel >= 0 && o.panel < K) {
+      if ((e = cudaEventRecord(comm->ev_panel[o.panel], os)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+      has[o.panel] = true;
     }
   }
-  // (2) the lifted compute: this rank's rows of C (Fig. 4, k = rank), panel by panel.
-  //     Panel j > 0 continues every element's fma chain from panel j-1's C, so the
-  //     result is bitwise the one-launch result ("the addition loop to add up the
-  //     blocks").
+  // the lifted compute: this rank's rows of C, panel by panel. Panel j > 0 continues
+  // every element's fma chain from panel j-1's C, so the result is bitwise the
+  // one-launch result ("the addition loop to add up the blocks").
   for (int j = 0; j < K; ++j) {
     const int64_t k0 = bnd[j], k1 = bnd[j + 1];
-    if (K > 1)
-      if ((e = cudaStreamWaitEvent(s, comm->ev_panel[j], 0)) != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
+    if (has[j] && (e = cudaStreamWaitEvent(s, comm->ev_panel[j], 0)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamWaitEvent");
     if (k1 <= k0 && j > 0) continue;
     GemmArgs g{rows, k1 - k0, p, (const char*)A_local + k0 * es, (const char*)B + k0 * p * es, C_local,
                n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
     if (j == K - 1) g.peers = last_peers;  // the final panel writes the final C
-    // panels that run while later panels are still being broadcast leave SMs free
-    if ((rc = gemm_reserving(g, dtype, s, j < K - 1 ? kPipeCTAs : 0))) return rc;
+    if ((rc = gemm_reserving(g, dtype, s, reserve_sms && j < K - 1 ? kPipeCTAs : 0))) return rc;
+  }
+  // phase 2: gather of C (reading R14) / exit barrier
+  int group = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const auto& o = ops[i];
+    if (o.phase != 2) continue;
+    if (o.group != group) {
+      if (group && ncclGroupEnd() != ncclSuccess) return nccl_fail(ncclInternalError, "ncclGroupEnd");
+      if (o.group && ncclGroupStart() != ncclSuccess) return nccl_fail(ncclInternalError, "ncclGroupStart");
+      group = o.group;
+    }
+    const void* send = o.op == MOA_COLL_ALLGATHER ? C_local : (o.root == comm->rank ? C_local : nullptr);
+    if ((rc = issue_nccl(comm, o, o.op == MOA_COLL_BARRIER ? nullptr : C_full, send, dtype, s))) {
+      if (group) ncclGroupEnd();
+      return rc;
+    }
+  }
+  if (group) {
+    ncclResult_t r = ncclGroupEnd();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+  }
+  if ((flags & MOA_XF_GATHER) && !(flags & MOA_XF_FUSED_GATHER) && G == 1 && m * p > 0) {
+    e = cudaMemcpyAsync(C_full, C_local, (size_t)(m * p * es), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(C_full)");
   }
   return MOA_OK;
+}
+
+static bool overlap_bytes(const void* x, int64_t xb, const void* y, int64_t yb) {
+  if (!x || !y || xb <= 0 || yb <= 0) return false;
+  uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
+  return a0 < b1 && b0 < a1;
 }
 
 int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
@@ -1002,47 +1326,17 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
     set_error("C_full not aligned to the element size");
     return MOA_ERR_MISALIGNED;
   }
-  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
-    if (!x || !y || xb <= 0 || yb <= 0) return false;
-    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
-    return a0 < b1 && b0 < a1;
-  };
-  if (C_full && (overlap(C_full, m * p * es, B, n * p * es) || overlap(C_full, m * p * es, A_local, rows * n * es) ||
-                 overlap(C_full, m * p * es, C_local, rows * p * es))) {
+  if (C_full && (overlap_bytes(C_full, m * p * es, B, n * p * es) || overlap_bytes(C_full, m * p * es, A_local, rows * n * es) ||
+                 overlap_bytes(C_full, m * p * es, C_local, rows * p * es))) {
     set_error("C_full overlaps another operand");
     return MOA_ERR_ALIASING;
   }
-  cudaStream_t s = (cudaStream_t)stream;
-  if ((rc = lifted_bcast_compute(n, p, rows, A_local, B, C_local, dtype, s, comm, npanels, nullptr))) return rc;
-  const ncclDataType_t ty = nccl_type(dtype);
-  cudaError_t e;
-  // (3) optional gather of C (reading R14).
-  if (C_full && m * p > 0) {
-    if (comm->nranks == 1) {
-      e = cudaMemcpyAsync(C_full, C_local, (size_t)(m * p * es), cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(C_full)");
-    } else if (m % comm->nranks == 0) {
-      ncclResult_t r = ncclAllGather(C_local, C_full, (size_t)(rows * p), ty, comm->nccl, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(C)");
-    } else {
-      ncclResult_t r = ncclGroupStart();
-      for (int g = 0; g < comm->nranks && r == ncclSuccess; ++g) {
-        int64_t r0, rg;
-        moa_lift_rows(m, comm->nranks, g, &r0, &rg);
-        if (rg == 0) continue;
-        r = ncclBroadcast(g == comm->rank ? C_local : nullptr, (char*)C_full + r0 * p * es, (size_t)(rg * p), ty, g,
-                          comm->nccl, s);
-      }
-      ncclResult_t r2 = ncclGroupEnd();
-      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(C block)");
-      if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
-    }
-  }
-  return MOA_OK;
+  // B inside a symmetric window (every rank): the exchange is copy-engine pulls
+  int flags = C_full ? MOA_XF_GATHER : 0;
+  if (comm->nranks > 1 && n * p > 0 && find_window(comm, B, n * p * es)) flags |= MOA_XF_PULL_B;
+  return lifted_rows_exec(m, n, p, rows, A_local, B, C_local, C_full, dtype, (cudaStream_t)stream, comm, npanels,
+                          flags, nullptr);
 }
-
-static const moa_comm_s::Window* find_window(moa_comm_t comm, const void* ptr, int64_t bytes);
-static int stream_barrier(moa_comm_t comm, cudaStream_t s);
 
 int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,
                          void* workspace, int dtype, void* stream, moa_comm_t comm) {
@@ -1054,45 +1348,39 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
     set_error("negative extent");
     return MOA_ERR_INVALID_SHAPE;
   }
+  const int G = comm->nranks;
   int64_t col0 = 0, cols = 0;
-  int rc = moa_lift_rows(p, comm->nranks, comm->rank, &col0, &cols);  // the split of the j axis
+  int rc = moa_lift_rows(p, G, comm->rank, &col0, &cols);  // the split of the j axis
   if (rc) return rc;
   if ((rc = validate(m, n, cols, A, B_local, C_local, dtype))) return rc;
   const int64_t es = elem_size(dtype);
-  // C_full inside a symmetric window (moa_comm_alloc_window), fp64: the gather is fused
-  // into the GEMM epilogue — this rank's column block is computed straight into its
-  // columns of C_full (row stride p) and stored by the same epilogue into every
+  // C_full inside a symmetric window (moa_comm_alloc_window), fp64/fp32: the gather is
+  // fused into the GEMM epilogue — this rank's column block is computed straight into
+  // its columns of C_full (row stride p) and stored by the same epilogue into every
   // peer's C_full over NVLink; no workspace, no per-rank broadcasts of C.
   const moa_comm_s::Window* win =
-      (C_full && m * p > 0 && (dtype == MOA_F64 || dtype == MOA_F32) && comm->nranks - 1 <= kMaxPeerDst) ? find_window(comm, C_full, m * p * es)
-                                                                                  : nullptr;
+      (C_full && m * p > 0 && (dtype == MOA_F64 || dtype == MOA_F32) && G - 1 <= kMaxPeerDst)
+          ? find_window(comm, C_full, m * p * es)
+          : nullptr;
   if (C_full && m * p > 0 && !win) {
     if ((reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
       set_error("C_full not aligned to the element size");
       return MOA_ERR_MISALIGNED;
     }
-    if (comm->nranks > 1 && !workspace) {
+    if (G > 1 && !workspace) {
       set_error("gathering column blocks needs a workspace of m * ceil(p / G) elements");
       return MOA_ERR_NULL_POINTER;
     }
   }
+  const int flags = win ? MOA_XF_FUSED_GATHER : (C_full && m * p > 0 ? MOA_XF_GATHER : 0);
+  const std::vector<moa_coll_t> ops = plan_vec(MOA_XPLAN_COLS, m, n, p, dtype, G, comm->rank, 0, 0, 0, flags);
   cudaStream_t s = (cudaStream_t)stream;
-  const ncclDataType_t ty = nccl_type(dtype);
-  // (1) every processor needs all of A (ip_cols.c reads A[(i*shr0)+sigma] with no
-  //     column-group index): in-place broadcast from rank 0.
-  if (m * n > 0 && comm->nranks > 1) {
-    ncclResult_t r = ncclBroadcast(A, A, (size_t)(m * n), ty, 0, comm->nccl, s);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(A)");
-  }
+  for (const auto& o : ops)  // phase 0: (entry barrier,) the broadcast of A
+    if (o.phase == 0 && (rc = issue_nccl(comm, o, A, nullptr, dtype, s))) return rc;
   if (win) {
-    if ((rc = stream_barrier(comm, s))) return rc;  // entry: every rank reached this call
-    if (m * n > 0 && comm->nranks > 1) {
-      ncclResult_t r = ncclBroadcast(A, A, (size_t)(m * n), ty, 0, comm->nccl, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(A)");
-    }
     PeerDst pd{};
     const uintptr_t off = (uintptr_t)C_full - (uintptr_t)win->ptr + (uintptr_t)(col0 * es);
-    for (int r = 0; r < comm->nranks; ++r)
+    for (int r = 0; r < G; ++r)
       if (r != comm->rank && cols > 0) pd.dst[pd.nd++] = (char*)win->peer[(size_t)r] + off;
     GemmArgs g{m, n, cols, A, B_local, (char*)C_full + col0 * es, n > 0 ? n : 1, cols > 0 ? cols : 1, p, 0};
     g.peers = &pd;
@@ -1102,28 +1390,30 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
                                         (size_t)(cols * es), (size_t)m, cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_local)");
     }
-    return stream_barrier(comm, s);  // exit: every rank's epilogue stores are complete
+  } else if ((rc = moa_gemm(m, n, cols, A, B_local, C_local, dtype, stream))) {
+    // this rank's column block: C[:, col0:col0+cols] = A • B[:, col0:col0+cols]
+    return rc;
   }
-  // (2) this rank's column block: C[:, col0:col0+cols] = A • B[:, col0:col0+cols].
-  if ((rc = moa_gemm(m, n, cols, A, B_local, C_local, dtype, stream))) return rc;
-  // (3) optional gather: rank r's block travels (broadcast) into the workspace, then
-  //     a strided 2-D copy places it at columns [col0_r, col0_r + cols_r) of C_full.
-  if (C_full && m * p > 0) {
-    for (int g = 0; g < comm->nranks; ++g) {
-      int64_t c0, cg;
-      moa_lift_rows(p, comm->nranks, g, &c0, &cg);
-      if (cg == 0) continue;
-      const void* src = C_local;
-      if (comm->nranks > 1) {
-        ncclResult_t r = ncclBroadcast(g == comm->rank ? C_local : nullptr, workspace, (size_t)(m * cg), ty, g,
-                                       comm->nccl, s);
-        if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(C column block)");
-        src = workspace;
-      }
-      cudaError_t e = cudaMemcpy2DAsync((char*)C_full + c0 * es, (size_t)(p * es), src, (size_t)(cg * es),
-                                        (size_t)(cg * es), (size_t)m, cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_full)");
+  // phase 2: (exit barrier) or rank g's block through the workspace, then a strided
+  // 2-D copy places it at columns [col0_g, col0_g + cols_g) of C_full
+  for (const auto& o : ops) {
+    if (o.phase != 2) continue;
+    if (o.op == MOA_COLL_BARRIER) {
+      if ((rc = stream_barrier(comm, s))) return rc;
+      continue;
     }
+    moa_coll_t w = o;
+    w.offset = 0;  // the block lands at the start of the workspace
+    if ((rc = issue_nccl(comm, w, workspace, o.root == comm->rank ? C_local : nullptr, dtype, s))) return rc;
+    const int64_t cg = o.count / (m > 0 ? m : 1);
+    cudaError_t e = cudaMemcpy2DAsync((char*)C_full + o.offset * es, (size_t)(p * es), workspace, (size_t)(cg * es),
+                                      (size_t)(cg * es), (size_t)m, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_full)");
+  }
+  if (!win && C_full && m * p > 0 && G == 1) {
+    cudaError_t e = cudaMemcpy2DAsync(C_full, (size_t)(p * es), C_local, (size_t)(cols * es), (size_t)(cols * es),
+                                      (size_t)m, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_full)");
   }
   return MOA_OK;
 }
@@ -1146,7 +1436,7 @@ static int lifted_2d_impl(int64_t m, int64_t n, int64_t p, int grid_rows, int gr
   if ((rc = validate(rows, n, cols, A_panel, B_panel, C_block, dtype))) return rc;
   const int64_t es = elem_size(dtype);
   const moa_comm_s::Window* win = nullptr;
-  if (C_full && m * p > 0) {  // the fused gather: C_full must be a symmetric window, fp64
+  if (C_full && m * p > 0) {  // the fused gather: C_full must be a symmetric window
     if (dtype != MOA_F64 && dtype != MOA_F32) {
       set_error("moa_gemm_lifted_2d_gather: MOA_F64 or MOA_F32 only");
       return MOA_ERR_INVALID_DTYPE;
@@ -1161,28 +1451,12 @@ static int lifted_2d_impl(int64_t m, int64_t n, int64_t p, int grid_rows, int gr
     }
   }
   cudaStream_t s = (cudaStream_t)stream;
-  const ncclDataType_t ty = nccl_type(dtype);
-  if (win && (rc = stream_barrier(comm, s))) return rc;  // entry: every rank reached this call
-  if (comm->nranks > 1) {
-    if (comm->grid_rows != grid_rows || comm->grid_cols != grid_cols) {  // (re)split, collective
-      if (comm->row_comm) ncclCommDestroy(comm->row_comm);
-      if (comm->col_comm) ncclCommDestroy(comm->col_comm);
-      comm->row_comm = comm->col_comm = nullptr;
-      ncclResult_t q = ncclCommSplit(comm->nccl, r, c, &comm->row_comm, nullptr);
-      if (q == ncclSuccess) q = ncclCommSplit(comm->nccl, c, r, &comm->col_comm, nullptr);
-      if (q != ncclSuccess) return nccl_fail(q, "ncclCommSplit");
-      comm->grid_rows = grid_rows;
-      comm->grid_cols = grid_cols;
-    }
-    // A's row panel travels along the process row (root: column 0), B's column panel
-    // along the process column (root: row 0): the i axis lifted over grid rows, the
-    // j axis over grid columns (Figs. 4 and 5 together).
-    ncclResult_t q = ncclSuccess;
-    if (grid_cols > 1 && rows * n > 0) q = ncclBroadcast(A_panel, A_panel, (size_t)(rows * n), ty, 0, comm->row_comm, s);
-    if (q == ncclSuccess && grid_rows > 1 && n * cols > 0)
-      q = ncclBroadcast(B_panel, B_panel, (size_t)(n * cols), ty, 0, comm->col_comm, s);
-    if (q != ncclSuccess) return nccl_fail(q, "ncclBroadcast(2-D panels)");
-  }
+  const std::vector<moa_coll_t> ops = plan_vec(MOA_XPLAN_2D, m, n, p, dtype, comm->nranks, comm->rank, grid_rows,
+                                               grid_cols, 0, win ? MOA_XF_FUSED_GATHER : 0);
+  if (comm->nranks > 1 && (rc = split_2d(comm, grid_rows, grid_cols))) return rc;  // collective, cached
+  for (const auto& o : ops)
+    if (o.phase == 0 && (rc = issue_nccl(comm, o, o.operand == MOA_OPERAND_A ? A_panel : B_panel, nullptr, dtype, s)))
+      return rc;
   if (!win) return moa_gemm(rows, n, cols, A_panel, B_panel, C_block, dtype, stream);
   // fused gather: the block is computed into C_full at (row0, col0) with row stride p
   // and stored by the same epilogue into every other rank's C_full at that offset
@@ -1199,7 +1473,9 @@ static int lifted_2d_impl(int64_t m, int64_t n, int64_t p, int grid_rows, int gr
                                       (size_t)(p * es), (size_t)(cols * es), (size_t)rows, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync(C_block)");
   }
-  return stream_barrier(comm, s);  // exit: every rank's epilogue stores are complete
+  for (const auto& o : ops)  // exit barrier: every rank's epilogue stores are complete
+    if (o.phase == 2 && (rc = issue_nccl(comm, o, nullptr, nullptr, dtype, s))) return rc;
+  return MOA_OK;
 }
 
 int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel, void* B_panel,
@@ -1219,6 +1495,28 @@ int moa_gemm_lifted_2d_gather(int64_t m, int64_t n, int64_t p, int grid_rows, in
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                     int dtype, void* stream, moa_comm_t comm) {
   return moa_gemm_lifted_ex(m, n, p, A_local, B, C_local, C_full, dtype, stream, comm, 0);
+}
+
+int moa_comm_agree(moa_comm_t comm, int local_status, int* global_status) {
+  if (!comm || !global_status) {
+    set_error("NULL argument");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (comm->nranks <= 1) {
+    *global_status = local_status;
+    return MOA_OK;
+  }
+  int* d = comm->barrier_buf + 1;
+  cudaError_t e = cudaMemcpyAsync(d, &local_status, sizeof(int), cudaMemcpyHostToDevice, comm->side);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(agree)");
+  ncclResult_t r = ncclAllReduce(d, d, 1, ncclInt32, ncclMax, comm->nccl, comm->side);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(agree)");
+  int out = 0;
+  if ((e = cudaMemcpyAsync(&out, d, sizeof(int), cudaMemcpyDeviceToHost, comm->side)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(comm->side)) != cudaSuccess)
+    return cuda_fail(e, "agree");
+  *global_status = out;
+  return MOA_OK;
 }
 
 }  // extern "C"
@@ -1246,24 +1544,21 @@ int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda
   PeerDst pd{};
   pd.nd = m * p > 0 ? ndst : 0;
   const int64_t cb = m * p > 0 ? ((m - 1) * ldc + p) * es : 0;  // byte span of one strided m x p block
-  auto ov = [cb](const void* x, const void* y, int64_t yb) {
-    if (!x || !y || cb <= 0 || yb <= 0) return false;
-    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)cb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
-    return a0 < b1 && b0 < a1;
-  };
   for (int d = 0; d < pd.nd; ++d) {
     void* q = dst[d];
     if (!q) {
       set_error("NULL destination");
       return MOA_ERR_NULL_POINTER;
     }
+    // element alignment is the contract; 16-byte alignment (with C's) selects the TMA
+    // kernels' vector-store epilogue, anything else the generic kernels (tma_eligible)
     if (reinterpret_cast<uintptr_t>(q) % (uintptr_t)es) {
       set_error("destination not aligned to the element size");
       return MOA_ERR_MISALIGNED;
     }
     const int64_t ab = m * n > 0 ? ((m - 1) * lda + n) * es : 0, bb = n * p > 0 ? ((n - 1) * ldb + p) * es : 0;
-    bool bad = ov(q, A, ab) || ov(q, B, bb) || ov(q, C, cb);
-    for (int e2 = 0; e2 < d && !bad; ++e2) bad = ov(q, dst[e2], cb);
+    bool bad = overlap_bytes(q, cb, A, ab) || overlap_bytes(q, cb, B, bb) || overlap_bytes(q, cb, C, cb);
+    for (int e2 = 0; e2 < d && !bad; ++e2) bad = overlap_bytes(q, cb, dst[e2], cb);
     if (bad) {
       set_error("destination overlaps an operand or another destination");
       return MOA_ERR_ALIASING;
@@ -1298,11 +1593,6 @@ int moa_comm_alloc_window(moa_comm_t comm, size_t bytes, void** ptr) {
   cudaError_t e = cudaGetDevice(&guard.prev);
   if (e == cudaSuccess) e = cudaSetDevice(comm->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-  if (!comm->barrier_buf) {
-    RelaxedCapture relaxed_capture;
-    if ((e = cudaMalloc(&comm->barrier_buf, sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc(barrier)");
-    if ((e = cudaMemset(comm->barrier_buf, 0, sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMemset(barrier)");
-  }
   const size_t sz = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
   moa_comm_s::Window w;
   w.bytes = bytes;
@@ -1376,15 +1666,6 @@ static const moa_comm_s::Window* find_window(moa_comm_t comm, const void* ptr, i
   return nullptr;
 }
 
-// Barrier of the fused gather: a one-element all-reduce on the stream. When it
-// completes on rank r, every rank has finished the work it enqueued before it (for
-// the exit barrier: its GEMM, whose peer stores are complete at kernel end).
-static int stream_barrier(moa_comm_t comm, cudaStream_t s) {
-  if (comm->nranks <= 1) return MOA_OK;
-  ncclResult_t r = ncclAllReduce(comm->barrier_buf, comm->barrier_buf, 1, ncclInt32, ncclMax, comm->nccl, s);
-  return r == ncclSuccess ? MOA_OK : nccl_fail(r, "ncclAllReduce(barrier)");
-}
-
 int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_full, int dtype,
                            void* stream, moa_comm_t comm, int npanels) {
   if (!comm) {
@@ -1431,12 +1712,7 @@ int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local,
   }
   char* c_local = mp > 0 ? (char*)C_full + row0 * p * es : nullptr;
   if ((rc = validate(rows, n, p, A_local, B, c_local, dtype))) return rc;
-  auto overlap = [](const void* x, int64_t xb, const void* y, int64_t yb) {
-    if (!x || !y || xb <= 0 || yb <= 0) return false;
-    uintptr_t a0 = (uintptr_t)x, a1 = a0 + (uintptr_t)xb, b0 = (uintptr_t)y, b1 = b0 + (uintptr_t)yb;
-    return a0 < b1 && b0 < a1;
-  };
-  if (overlap(C_full, mp, B, n * p * es) || overlap(C_full, mp, A_local, rows * n * es)) {
+  if (overlap_bytes(C_full, mp, B, n * p * es) || overlap_bytes(C_full, mp, A_local, rows * n * es)) {
     set_error("C_full overlaps another operand");
     return MOA_ERR_ALIASING;
   }
@@ -1448,12 +1724,8 @@ int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local,
     for (int r = 0; r < comm->nranks; ++r)
       if (r != comm->rank) pd.dst[pd.nd++] = (char*)win->peer[(size_t)r] + off;
   }
-  cudaStream_t s = (cudaStream_t)stream;
-  // entry barrier: no rank stores into a peer's C_full before that peer has reached
-  // this call in its stream order (its earlier readers of C_full are done)
-  if ((rc = stream_barrier(comm, s))) return rc;
-  if ((rc = lifted_bcast_compute(n, p, rows, A_local, B, c_local, dtype, s, comm, npanels, pd.nd ? &pd : nullptr)))
-    return rc;
-  // exit barrier: every rank's GEMM (and so its peer stores) has completed
-  return stream_barrier(comm, s);
+  int flags = MOA_XF_FUSED_GATHER;
+  if (comm->nranks > 1 && n * p > 0 && find_window(comm, B, n * p * es)) flags |= MOA_XF_PULL_B;
+  return lifted_rows_exec(m, n, p, rows, A_local, B, c_local, nullptr, dtype, (cudaStream_t)stream, comm, npanels,
+                          flags, pd.nd ? &pd : nullptr);
 }

@@ -155,6 +155,6 @@ bool acquire_tile_counter(cudaStream_t stream, unsigned int** out);
 // Host: `count` zeroed split-tile flags for one stream-K launch (a window of a
 // per-device ring, zeroed once at creation; every launch leaves its flags at 0 —
 // see split_signal / split_wait). Returns false (error set) on failure.
-bool acquire_split_flags(unsigned int count, unsigned int** out);
+bool acquire_split_flags(unsigned int count, cudaStream_t stream, unsigned int** out);
 
 }  // namespace moa

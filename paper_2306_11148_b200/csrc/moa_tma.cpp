@@ -56,11 +56,34 @@ std::mutex g_ctr_mu;
 std::map<int, CounterPool> g_ctr;
 }  // namespace
 
+// A launch being captured into a CUDA graph keeps its slot addresses for every replay,
+// while eager launches keep cycling through the ring: after a wrap-around an eager
+// launch could share a counter (or split flags) with a replay running concurrently.
+// So captured launches get dedicated slots, allocated here and owned by the process
+// for its lifetime (graphs may outlive any scope the library could see).
+static bool capturing(cudaStream_t stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return stream && cudaStreamIsCapturing(stream, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+
+static cudaError_t dedicated_zeroed(size_t bytes, unsigned int** out) {
+  RelaxedCapture relaxed_capture;
+  cudaStream_t ps = nullptr;
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemsetAsync(*out, 0, bytes, ps);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ps);
+  if (ps) cudaStreamDestroy(ps);
+  return e;
+}
+
 bool acquire_tile_counter(cudaStream_t stream, unsigned int** out) {
   int device = 0;
   cudaError_t e = cudaGetDevice(&device);
   unsigned int* slot = nullptr;
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && capturing(stream)) {
+    e = dedicated_zeroed(sizeof(unsigned int), &slot);  // (the memset node below resets it per replay)
+  } else if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(g_ctr_mu);
     CounterPool& pool = g_ctr[device];
     if (!pool.dev) {  // library-owned, once (capture-safe: not stream work)
@@ -93,7 +116,7 @@ std::mutex g_flag_mu;
 std::map<int, FlagPool> g_flag;
 }  // namespace
 
-bool acquire_split_flags(unsigned int count, unsigned int** out) {
+bool acquire_split_flags(unsigned int count, cudaStream_t stream, unsigned int** out) {
   int device = 0;
   cudaError_t e = cudaGetDevice(&device);
   unsigned int* slot = nullptr;
@@ -101,7 +124,9 @@ bool acquire_split_flags(unsigned int count, unsigned int** out) {
     set_error("split flags: grid larger than the flag pool");
     return false;
   }
-  if (e == cudaSuccess) {
+  if (e == cudaSuccess && capturing(stream)) {
+    e = dedicated_zeroed(count * sizeof(unsigned int), &slot);  // self-resetting, as the ring's
+  } else if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(g_flag_mu);
     FlagPool& pool = g_flag[device];
     if (!pool.dev) {  // library-owned, once; capture-safe: zeroed on a private stream

@@ -1,0 +1,165 @@
+"""One rank of the multi-process lifted-path tests (tests/test_lifted_multiproc_gpu.py).
+
+Run as a separate process per rank, with the test-only NCCL stand-in
+(tests/nccl_shim, LD_PRELOAD) when several ranks share one GPU, or with real NCCL
+when every rank has a GPU of its own. For each case it drives one lifted entry point
+of libmoa.so through the product binding with REAL multi-rank semantics (every
+`nranks > 1` branch: broadcasts of B / A, pipelined k-panels on the split
+communicator, copy-engine pulls of B from rank 0's window, NCCL gathers, fused
+peer-store gathers into symmetric windows, 2-D row/column sub-communicators) and
+compares every output it holds with the CPU oracle (Fig. 3 ip.c, fused update —
+reading R3), bit for bit. Inputs a rank does not own start as NaN so that a missing
+exchange cannot pass. Results go to <out>/rank<r>.json; the stand-in's collective
+log goes to <out>/<case>.rank<r>.jsonl.
+
+    python tests/mp_lifted_worker.py RANK WORLD PORT OUT_DIR CASES_JSON [DEVICE]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import traceback
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    rank, world, port, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    cases = json.loads(open(sys.argv[5]).read())
+    device = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_11148_b200 as moa
+    from inputs import inputs as I
+    from oracle import oracle as O
+
+    torch.cuda.set_device(device)
+    dev = torch.device("cuda", device)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = moa.Comm(device=device)
+    results = {}
+
+    def t(a, dt):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt)
+
+    def nan(shape, dt):
+        return torch.full(shape, float("nan"), dtype=dt, device=dev)
+
+    for case in cases:
+        name = case["name"]
+        os.environ["MOA_NCCL_SHIM_LOG"] = os.path.join(out, f"{name}.rank{rank}.jsonl")
+        kind, m, n, p = case["kind"], case["m"], case["n"], case["p"]
+        npdt = np.float32 if case.get("dtype") == "f32" else np.float64
+        dt = torch.float32 if npdt == np.float32 else torch.float64
+        seed = case.get("seed", 7)
+        Ah = I.host_matrix(m, n, seed, I.ID_A, dtype=npdt)
+        Bh = I.host_matrix(n, p, seed, I.ID_B, dtype=npdt)
+        ref = O.ip(Ah, Bh, fused=True)
+        checks = {}
+        try:
+            dist.barrier()
+            if kind in ("rows", "rows_pull", "rows_fused", "rows_pull_fused", "rows_host"):
+                r0, rows = moa.lift_rows(m, world, rank)
+                A_local = t(Ah[r0:r0 + rows], dt)
+                pull = kind in ("rows_pull", "rows_pull_fused")
+                B = comm.alloc_window((n, p), dt) if pull else nan((n, p), dt)
+                if rank == 0:
+                    B.copy_(t(Bh, dt))
+                else:
+                    B.fill_(float("nan"))
+                torch.cuda.synchronize()
+                if kind in ("rows", "rows_pull"):
+                    C_local = nan((rows, p), dt)
+                    C_full = nan((m, p), dt) if case.get("gather") else None
+                    moa.gemm_lifted(m, A_local, B, C_local, comm, C_full=C_full, npanels=case.get("npanels", 0))
+                    torch.cuda.synchronize()
+                    checks["C_local"] = np.array_equal(C_local.cpu().numpy(), ref[r0:r0 + rows])
+                    if C_full is not None:
+                        checks["C_full"] = np.array_equal(C_full.cpu().numpy(), ref)
+                elif kind in ("rows_fused", "rows_pull_fused"):
+                    C_full = comm.alloc_window((m, p), dt)
+                    C_full.fill_(float("nan"))
+                    torch.cuda.synchronize()
+                    dist.barrier()  # every rank's window is initialised before any peer store
+                    moa.gemm_lifted_gather(m, A_local, B, C_full, comm, npanels=case.get("npanels", 0))
+                    torch.cuda.synchronize()
+                    checks["C_full"] = np.array_equal(C_full.cpu().numpy(), ref)
+                    dist.barrier()
+                    comm.free_window(C_full)
+                else:  # rows_host: host buffers, B on rank 0's host only
+                    hA = torch.from_numpy(np.ascontiguousarray(Ah[r0:r0 + rows])).pin_memory()
+                    hB = torch.from_numpy(Bh).pin_memory() if rank == 0 else None
+                    hC = torch.full((rows, p), float("nan"), dtype=dt).pin_memory()
+                    Ad, Cd = nan((rows, n), dt), nan((rows, p), dt)
+                    moa.gemm_lifted_host(m, hA, hB, hC, Ad, B, Cd, comm)
+                    checks["C_host"] = np.array_equal(hC.numpy(), ref[r0:r0 + rows])
+                checks["B"] = np.array_equal(B.cpu().numpy(), Bh)
+                if pull:
+                    dist.barrier()
+                    comm.free_window(B)
+            elif kind in ("cols", "cols_fused"):
+                c0, cols = moa.lift_rows(p, world, rank)
+                A = t(Ah, dt) if rank == 0 else nan((m, n), dt)
+                B_local = t(Bh[:, c0:c0 + cols], dt)
+                C_local = nan((m, cols), dt)
+                if kind == "cols_fused":
+                    C_full = comm.alloc_window((m, p), dt)
+                    C_full.fill_(float("nan"))
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    moa.gemm_lifted_cols(A, B_local, C_local, p, comm, C_full=C_full)
+                else:
+                    C_full = nan((m, p), dt) if case.get("gather") else None
+                    ws = nan((m * (-(-p // world)),), dt) if case.get("gather") else None
+                    moa.gemm_lifted_cols(A, B_local, C_local, p, comm, C_full=C_full, workspace=ws)
+                torch.cuda.synchronize()
+                checks["A"] = np.array_equal(A.cpu().numpy(), Ah)
+                checks["C_local"] = np.array_equal(C_local.cpu().numpy(), ref[:, c0:c0 + cols])
+                if C_full is not None:
+                    checks["C_full"] = np.array_equal(C_full.cpu().numpy(), ref)
+                if kind == "cols_fused":
+                    dist.barrier()
+                    comm.free_window(C_full)
+            elif kind in ("2d", "2d_fused"):
+                gr, gc = case["grid"]
+                r, c = divmod(rank, gc)
+                row0, rows = moa.lift_rows(m, gr, r)
+                col0, cols = moa.lift_rows(p, gc, c)
+                A_panel = t(Ah[row0:row0 + rows], dt) if c == 0 else nan((rows, n), dt)
+                B_panel = t(Bh[:, col0:col0 + cols], dt) if r == 0 else nan((n, cols), dt)
+                C_block = nan((rows, cols), dt)
+                C_full = None
+                if kind == "2d_fused":
+                    C_full = comm.alloc_window((m, p), dt)
+                    C_full.fill_(float("nan"))
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                moa.gemm_lifted_2d(m, p, gr, gc, A_panel, B_panel, C_block, comm, C_full=C_full)
+                torch.cuda.synchronize()
+                checks["A_panel"] = np.array_equal(A_panel.cpu().numpy(), Ah[row0:row0 + rows])
+                checks["B_panel"] = np.array_equal(B_panel.cpu().numpy(), Bh[:, col0:col0 + cols])
+                checks["C_block"] = np.array_equal(C_block.cpu().numpy(), ref[row0:row0 + rows, col0:col0 + cols])
+                if C_full is not None:
+                    checks["C_full"] = np.array_equal(C_full.cpu().numpy(), ref)
+                    dist.barrier()
+                    comm.free_window(C_full)
+            else:
+                raise ValueError(f"unknown case kind {kind}")
+            results[name] = {"ok": all(checks.values()), "checks": checks}
+        except Exception as e:  # report, keep the ranks in step for the next case
+            results[name] = {"ok": False, "error": f"{type(e).__name__}: {e}", "tb": traceback.format_exc()}
+        dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+    with open(os.path.join(out, f"rank{rank}.json"), "w") as f:
+        json.dump(results, f)
+
+
+if __name__ == "__main__":
+    main()

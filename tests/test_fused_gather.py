@@ -282,3 +282,28 @@ def test_lifted_cols_and_2d_fused_gather_single_rank(cuda_device):
     finally:
         comm.close()
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,offsets", [(torch.float64, [1]), (torch.float32, [1, 2, 3])])
+def test_scatter_destination_not_16B_aligned(cuda_device, dtype, offsets):
+    """Regression (round-1 review): a destination aligned to its element but not to 16
+    bytes (fp64 at base+8; fp32 at base+4/+8/+12) on a TMA-eligible shape used to
+    select K1/K3, whose epilogue stores 16-byte vectors: a misaligned-address fault.
+    Such a destination now routes the call to the generic kernel; every destination
+    and C hold the oracle's bits."""
+    m, n, p = 256, 64, 192                       # TMA-eligible: the chooser would pick K1 / K3
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    Ah = I.host_matrix(m, n, 4, I.ID_A, dtype=npdt)
+    Bh = I.host_matrix(n, p, 4, I.ID_B, dtype=npdt)
+    ref = O.ip(Ah, Bh, fused=True)
+    A, B = torch.from_numpy(Ah).to(cuda_device), torch.from_numpy(Bh).to(cuda_device)
+    for off in offsets:
+        C = torch.full((m, p), float("nan"), dtype=dtype, device=cuda_device)
+        buf = torch.full((m * p + 8,), float("nan"), dtype=dtype, device=cuda_device)
+        dst = buf[off:off + m * p].view(m, p)       # element-aligned, not 16-B aligned
+        assert dst.data_ptr() % 16 != 0
+        moa.gemm_scatter(A, B, C, [dst])
+        torch.cuda.synchronize()
+        assert np.array_equal(C.cpu().numpy(), ref), off
+        assert np.array_equal(dst.cpu().numpy(), ref), off

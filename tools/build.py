@@ -6,6 +6,7 @@ Targets:
   inputs       inputs/libmoa_inputs.so         gcc (host input generator)
   inputs_cuda  inputs/libmoa_inputs_cuda.so    nvcc sm_100a (device input generator)
   moa          paper_2306_11148_b200/libmoa.so nvcc sm_100a (the product: C-ABI + kernels, links NCCL)
+  shim         tests/nccl_shim/libmoa_nccl_shim.so  test-only NCCL stand-in (several ranks on one GPU)
   all          everything (default)
 
 Incremental: a target is rebuilt only when a source/header is newer than its output
@@ -109,7 +110,21 @@ def build_moa(force=False, verbose_ptxas=False):
     return out
 
 
-TARGETS = {"oracle": build_oracle, "inputs": build_inputs, "inputs_cuda": build_inputs_cuda, "moa": build_moa}
+def build_shim(force=False):
+    """tests/nccl_shim/libmoa_nccl_shim.so: TEST INFRASTRUCTURE (an LD_PRELOAD stand-in for
+    the NCCL subset libmoa.so calls, so several processes can share one GPU in the
+    multi-rank tests). Never linked into the product."""
+    src = os.path.join(ROOT, "tests", "nccl_shim", "moa_nccl_shim.cu")
+    out = os.path.join(ROOT, "tests", "nccl_shim", "libmoa_nccl_shim.so")
+    nccl = _nccl_root()
+    if force or _stale(out, [src]):
+        _run([NVCC, *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(nccl, "include"),
+              src, "-o", out, "-L/usr/local/cuda/lib64/stubs", "-lcuda", "-lcudart"])
+    return out
+
+
+TARGETS = {"oracle": build_oracle, "inputs": build_inputs, "inputs_cuda": build_inputs_cuda, "moa": build_moa,
+           "shim": build_shim}
 
 
 def main(argv=None):
