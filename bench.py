@@ -1,34 +1,44 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 MoA-ONF fp64 GEMM (arXiv 2306.11148) — driver contract.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl moa|reference] [--N 8192]
-    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: row-lifted path)
+    python bench.py [--gpus G] [--steps K] [--warmup W] [--impl moa|reference] [--N 32768]
+    torchrun --nproc-per-node G bench.py --gpus G ...   (the same; bench.py self-launches
+                                                          its G ranks when WORLD_SIZE is unset)
 
-One "step" = one C := A • B (Eq. 3) over inputs resident in HBM.
-N = 1: square fp64 GEMM m = n = p = 8192 (BASELINE configs[1], the top of the
-paper's energy-vs-N sweep shape), through moa_gemm.
-N > 1: the row-lifted path (moa_gemm_lifted): rank g owns 8192 rows of A and C
-(weak scaling: m = 8192·N), n = p = 8192, B is broadcast from rank 0 over NVLink
-with NCCL every step (the path's one real exchange, reading R13).
---gather nccl|fused adds the optional all-gather of C (reading R14): ncclAllGather
-after the GEMM, or fused into the GEMM epilogue (moa_gemm_lifted_gather: NVLink
-peer stores into NCCL symmetric windows). --lifted runs the lifted path at N = 1
-too (a 1-rank NCCL communicator), which exercises the N > 1 code on one GPU.
+Workload: BASELINE configs[4] — the row-lifted fp64 GEMM m = n = p = 32768 on G B200
+("Dimension lifting over the rows of A and C ... assigns an index to
+processors"; Fig. 4 ip_rows.c P:150-171), STRONG scaling: the total problem is fixed
+and rank g owns rows moa_lift_rows(32768, G, g) of A and C. One "step" is one
+C := A • B (Eq. 3) through moa_gemm_lifted with inputs resident in HBM:
+B travels from rank 0 to every rank each step (P:165 — B carries no processor index),
+then each rank computes its rows. At G = 1 the same call runs on a 1-rank
+communicator (nothing travels).
 
-Rank 0 prints ONE JSON line: value = GFLOP/s of the whole job (all ranks' flops
-÷ the max-over-ranks device time of exactly K steps), plus roofline (DMMA fp64
-tensor peak), e2e (the same metric through moa_gemm_host / host buffers with the
-H2D and D2H copies inside the timed region), cpu_baseline (the oracle on this
-host's cores on a bounded row sample), energy (NVML joules per GEMM), an N sweep
-(GFLOP/s and J/GEMM vs N, the paper's time/energy-vs-N study), clocks.
+The exchange of B (G > 1): copy-engine pulls of B's k-panels from rank 0's symmetric
+window over NVLink (moa_pull_panels; no SMs taken from the GEMM), overlapped with the
+k-panel chain of the rank's GEMM. The NCCL-broadcast exchange (pipelined k-panels on a
+CTA-limited communicator) is measured beside it in "exchange_variants"; if the pulled
+exchange fails on a box, the NCCL one is the headline and the line says so.
+
+Rank 0 prints ONE JSON line: value = GFLOP/s of the whole job (2·m·n·p per step ÷ the
+max-over-ranks device time of exactly K steps), with the per-step component breakdown
+(compute alone, exchange alone, exposed exchange), roofline (the K1 DMMA kernel on the
+rank's rows), e2e (the same metric through moa_gemm_host / moa_gemm_lifted_host with
+host buffers, copies inside the timed region), energy (NVML J per GEMM summed over
+ranks, raw and idle-subtracted), at G = 1 the paper's time/energy-vs-N sweep (1024 …
+8192, 16000 = the paper's largest N, 16384 = the north_star's target; ≥ 3 windows of
+≥ 1 s each) with the fitted energy exponent, cpu_baseline (the oracle on this host's
+cores on a bounded row sample) and clocks.
 """
 from __future__ import annotations
 
 import argparse
 import faulthandler
 import json
+import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -38,46 +48,50 @@ sys.path.insert(0, ROOT)
 
 # fp64 tensor-core (DMMA.8x8x4) peak measured on this pool's B200 by tools/probe
 # (profiles/r01_fp64_probe.jsonl: 37.0 TF/s at 1965 MHz, flat from 4 to 32 warps/SM,
-# held for a 125 ms sustained run). MEASURED_PEAKS.json carries no fp64 figure.
+# held for a 125 ms sustained run; = 148 SM x 64 FMA/clk x 2 x 1.965 GHz within 0.5%).
+# MEASURED_PEAKS.json carries no fp64 figure.
 FP64_DMMA_PEAK_TFLOPS = 37.0
-FP64_PEAK_SOURCE = "measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_probe.jsonl (MEASURED_PEAKS.json has no fp64 entry)"
+FP64_PEAK_SOURCE = ("measured DMMA.8x8x4 microbenchmark, profiles/r01_fp64_probe.jsonl (MEASURED_PEAKS.json has no "
+                    "fp64 entry); nominal at the sampled SM clock in nominal_at_clock")
 METRIC = "fp64 GEMM GFLOP/s (joules/GEMM vs N in energy/sweep)"
 DATA = "synthetic (seeded splitmix64 uniform[-1,1), inputs/)"
+WORKLOAD_N = 32768
 
 
-def workload_config(N, ws, lifted=False, gather="none"):
+def workload_config(N, G, exchange="pull"):
     """The config object both arms report (same workload, same keys)."""
-    rows = N
-    m_total = rows * ws
-    lifted = lifted or ws > 1
-    gtxt = {"none": "", "nccl": ", C all-gathered with NCCL after the GEMM",
-            "fused": ", C all-gathered inside the GEMM epilogue (NVLink peer stores)"}[gather]
-    return {"workload": f"square fp64 GEMM m=n=p={N} per GPU (BASELINE configs[1], top of the 1024-8192 sweep)"
-                        + ("" if not lifted else f"; row-lifted over {ws} GPUs, m={m_total}, NCCL broadcast of B each step"
-                           + gtxt),
-            "m": m_total, "n": N, "p": N, "rows_per_rank": rows,
-            "parallelism": "single GPU" if not lifted else
-            f"row-lifted x{ws} ({'moa_gemm_lifted_gather' if gather == 'fused' else 'moa_gemm_lifted'})",
-            "gather": gather,
-            "l2": f"inputs larger than L2 ({(rows * N + N * N + rows * N) * 8 / 2**20:.0f} MiB resident vs 126 MB L2), no flush"}
+    rows = []
+    for g in range(G):
+        q, r = divmod(N, G)
+        rows.append(q + (1 if g < r else 0))
+    ex = {"pull": "copy-engine pulls of B's k-panels from rank 0's symmetric window over NVLink (moa_pull_panels), "
+                  "overlapped with the k-panel chain of each rank's GEMM",
+          "nccl": "NCCL broadcast of B in pipelined k-panels (moa_lift_panels) on a CTA-limited communicator",
+          "none": "none (one rank)"}[exchange if G > 1 else "none"]
+    return {"workload": f"row-lifted fp64 GEMM m=n=p={N} on {G} B200 (BASELINE configs[4]), strong scaling: rank g "
+                        f"owns rows moa_lift_rows({N}, {G}, g) of A and C; B ({N * N * 8 / 2 ** 30:.3g} GiB) travels "
+                        "from rank 0 to every rank each step",
+            "m": N, "n": N, "p": N, "rows_per_rank": rows, "parallelism": f"row-lifted x{G} (moa_gemm_lifted)",
+            "exchange": ex, "gather": "none (reading R14: the gather of C is optional)",
+            "l2": f"inputs larger than L2 ({(rows[0] * N * 2 + N * N) * 8 / 2 ** 30:.1f} GiB resident per GPU vs "
+                  "126 MB L2), no flush"}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["moa", "reference"], default="moa")
-    ap.add_argument("--N", type=int, default=8192, help="square size per rank (rows per rank = N)")
+    ap.add_argument("--N", type=int, default=WORKLOAD_N, help="m = n = p (default: BASELINE configs[4], 32768)")
+    ap.add_argument("--exchange", choices=["pull", "nccl"], default="pull")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep-sizes", default="1024,1536,2048,3072,4096,6144,8192")
-    ap.add_argument("--lifted", action="store_true",
-                    help="use the row-lifted (communicator) path even at N=1 (a 1-rank NCCL communicator)")
-    ap.add_argument("--gather", choices=["none", "nccl", "fused"], default="none",
-                    help="lifted path: also all-gather C (after the GEMM with NCCL, or fused into its epilogue)")
-    return ap.parse_args()
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--sweep-sizes", default="1024,1536,2048,3072,4096,6144,8192,16000,16384")
+    ap.add_argument("--sweep-windows", type=int, default=3)
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------- helpers --
@@ -94,7 +108,6 @@ class ClockSampler:
     def __init__(self, device_index: int, period: float = 0.05):
         self.ok = False
         self.samples = []
-        self.reasons = 0
         self.period = period
         try:
             import pynvml
@@ -140,6 +153,7 @@ class ClockSampler:
 
     def __enter__(self):
         if self.ok:
+            self.samples = []
             self._stop = threading.Event()
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
@@ -163,7 +177,7 @@ class ClockSampler:
                 "temp_c_median": statistics.median(s[3] for s in loaded), "temp_c_max": max(s[3] for s in loaded),
                 "samples": len(loaded)}
 
-    def idle_watts(self, seconds: float = 1.0):
+    def idle_watts(self, seconds: float = 2.0):
         """Idle-power baseline: NVML energy over a quiet window (J/s)."""
         e0 = self.energy_mj()
         if e0 is None:
@@ -179,6 +193,29 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def self_launch(args, argv) -> int:
+    """bench.py --gpus G without torchrun: start G ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1 and pass rank 0's one JSON line through.
+    Fails loudly when fewer than G GPUs are visible (MOA_BENCH_SHARE_GPU=1 lets the
+    ranks share cuda:0 — for the one-GPU test of this code path with the test-only
+    NCCL stand-in, never for a measurement)."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and os.environ.get("MOA_BENCH_SHARE_GPU") != "1":
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}\n")
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"), *argv]
+    sys.stdout.flush()
+    r = subprocess.run(cmd, cwd=ROOT, stdout=_JSON_FD if _JSON_FD is not None else None)
+    return r.returncode
 
 
 # ------------------------------------------------------------ cpu baseline --
@@ -226,8 +263,7 @@ def run_reference(args):
     from inputs import inputs as I
     from oracle import oracle as O
     N = args.N
-    m = N * max(1, args.gpus)
-    n = p = N
+    m = n = p = N
     cores = os.cpu_count() or 1
     B = I.host_matrix(n, p, 1, I.ID_B)
     A1 = I.host_matrix(1, n, 1, I.ID_A)
@@ -235,7 +271,7 @@ def run_reference(args):
     O.ip_rowblock(A1, B)
     t_row = time.perf_counter() - t0
     total_budget = 150.0  # seconds for warmup + steps
-    want = int(total_budget * cores / max(t_row, 1e-6) / (args.steps + args.warmup))
+    want = int(total_budget * cores / max(t_row, 1e-6) / max(1, args.steps + args.warmup))
     rows_per_step, threads = _oracle_sample_rows(want, m, cores)
     A = I.host_matrix(rows_per_step, n, 1, I.ID_A)
     for _ in range(args.warmup):
@@ -245,14 +281,15 @@ def run_reference(args):
         O.ip_rows(A, B, threads)
     dt = time.perf_counter() - t0
     value = 2.0 * rows_per_step * n * p * args.steps / dt / 1e9
-    cfg = workload_config(N, max(1, args.gpus))
+    G = max(1, args.gpus)
+    cfg = workload_config(N, G, args.exchange)
     cfg["reference_sample"] = (f"each step runs the CPU oracle (Fig. 4 ip_rows.c over {threads} threads, literal "
                                f"unfused ip.c update) on a bounded sample of {rows_per_step} of the {m} rows; "
                                f"GFLOP/s = 2*rows*n*p / time")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4),
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(dt / max(1, args.steps) * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": cfg,
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
@@ -285,12 +322,22 @@ def emit(line: dict):
     os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
-def main():
+def _fit_exponent(pts):
+    xs = [math.log(x) for x, _ in pts]
+    ys = [math.log(y) for _, y in pts]
+    mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
+    return sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs)
+
+
+def main(argv=None):
     faulthandler.enable()
     _quiet_stdout()
-    args = parse()
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args, argv)
 
     import torch
     import torch.distributed as dist
@@ -298,157 +345,227 @@ def main():
     from inputs import inputs as I
 
     ws, rank, local = dist_env()
-    lifted = ws > 1 or args.lifted or args.gather != "none"
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if lifted:
-        if ws == 1:
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29517")
-            os.environ.setdefault("RANK", "0")
-            os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=dev)
+    if ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        return 2
+    shared = os.environ.get("MOA_BENCH_SHARE_GPU") == "1"
+    device = 0 if shared else local
+    if not shared and torch.cuda.device_count() <= device:
+        sys.stderr.write(f"bench.py: rank {rank} needs cuda:{device}, {torch.cuda.device_count()} visible\n")
+        return 2
+    torch.cuda.set_device(device)
+    dev = torch.device("cuda", device)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if ws == 1:
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    # control plane (barriers, max over ranks, the 128-byte NCCL id) over gloo; the
+    # data plane is libmoa's own communicator
+    dist.init_process_group("gloo")
     stream = torch.cuda.current_stream()
+    comm = moa.Comm(device=device)
+    G = comm.world
 
     N = args.N
-    n = p = N
-    rows = N                      # rows of A/C per rank (weak scaling)
-    m_total = rows * ws
-    row0 = rank * rows
+    m = n = p = N
+    row0, rows = moa.lift_rows(m, G, rank)
     A = torch.empty((rows, n), dtype=torch.float64, device=dev)
-    B = torch.empty((n, p), dtype=torch.float64, device=dev)
     C = torch.empty((rows, p), dtype=torch.float64, device=dev)
-    I.device_fill(A, 1, I.ID_A, row0=row0)
-    if rank == 0:
-        I.device_fill(B, 1, I.ID_B)
-    else:
-        B.zero_()
-    comm = moa.Comm() if lifted else None
-    C_full = None
-    if args.gather == "fused":
-        C_full = comm.alloc_window((m_total, p))       # NCCL symmetric window
-    elif args.gather == "nccl":
-        C_full = torch.empty((m_total, p), dtype=torch.float64, device=dev)
+    if rows:
+        I.device_fill(A, 1, I.ID_A, row0=row0)
 
-    def step():
-        if comm is None:
-            moa.gemm(A, B, out=C)
-        elif args.gather == "fused":
-            moa.gemm_lifted_gather(m_total, A, B, C_full, comm)
+    def make_B(kind):
+        Bt = comm.alloc_window((n, p)) if (kind == "pull" and G > 1) else torch.empty((n, p), dtype=torch.float64,
+                                                                                    device=dev)
+        if rank == 0:
+            I.device_fill(Bt, 1, I.ID_B)
         else:
-            moa.gemm_lifted(m_total, A, B, C, comm, C_full=C_full)
+            Bt.zero_()  # every other rank receives B through the exchange each step
+        return Bt
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
+    def free_B(Bt):
+        if G > 1 and Bt is not None and args.exchange == "pull" and Bt.data_ptr() in comm._windows:
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.free_window(Bt)
 
-    sampler = ClockSampler(local)
-    torch.cuda.synchronize()
-    idle_w = sampler.idle_watts(1.0)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if lifted:
+    exchange = args.exchange if G > 1 else "none"
+    fallback = None
+    B = make_B(exchange)
+    B_hold = {}
+
+    def step(Bt):
+        moa.gemm_lifted(m, A, Bt, C, comm)
+
+    def timed(fn, k):
+        """k calls of fn between a barrier + synchronize on both sides; device time (ms)
+        on the launching stream, max over ranks."""
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
         dist.barrier()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(k):
+            evs[i][0].record(stream)
+            fn()
+            evs[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        el = t0.elapsed_time(t1)
+        per = [a.elapsed_time(b) for a, b in evs]
+        return max_over_ranks(el), per
+
+    def max_over_ranks(x):
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # warm-up (and the fallback if the pulled exchange is refused on this box)
+    try:
+        for _ in range(args.warmup):
+            step(B)
+        torch.cuda.synchronize()
+    except moa.MoAError as e:
+        if exchange != "pull":
+            raise
+        fallback = f"pulled exchange failed ({e}); NCCL exchange is the headline"
+        sys.stderr.write("bench.py: " + fallback + "\n")
+        exchange = "nccl"
+        B = torch.empty((n, p), dtype=torch.float64, device=dev)
+        if rank == 0:
+            I.device_fill(B, 1, I.ID_B)
+        for _ in range(args.warmup):
+            step(B)
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(device)
+    idle_w = sampler.idle_watts(2.0)
+    idle_w_sum = sum_over_ranks(idle_w or 0.0) if idle_w is not None else None
     e0 = sampler.energy_mj()
     with sampler:
-        t_start.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-        e1 = sampler.energy_mj()
-    if lifted:
-        dist.barrier()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    per_step = [a.elapsed_time(b) for a, b in ev]
-    if ws > 1:
-        t = torch.tensor([elapsed_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
-    flops_step = 2.0 * m_total * n * p
+        elapsed_ms, per_step = timed(lambda: step(B), args.steps)
+    e1 = sampler.energy_mj()
+    clocks = sampler.summary()
+    flops_step = 2.0 * m * n * p
     value = flops_step * args.steps / (elapsed_ms / 1e3) / 1e9  # GFLOP/s whole job
 
-    # dominant kernel (the GEMM itself) on the launching stream; on the lifted path the
-    # step also holds the B broadcast (and any gather), so time moa_gemm alone on this
-    # rank's rows afterwards.
-    if lifted:
-        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
-        for a, b in kev:
-            a.record(stream)
+    # components on each rank (max over ranks): compute alone (moa_gemm on the rank's
+    # rows, the dominant kernel), exchange alone (the same lifted call with no rows:
+    # B's exchange plan and nothing else), exposed exchange = step - compute
+    kreps = 3 if N >= 16384 else 5
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kreps)]
+    torch.cuda.synchronize()
+    for a, b in kev:
+        a.record(stream)
+        if rows:
             moa.gemm(A, B, out=C)
-            b.record(stream)
-        torch.cuda.synchronize()
-        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-    else:
-        kern_ms = statistics.mean(per_step)
+        b.record(stream)
+    torch.cuda.synchronize()
+    gemm_ms_rank = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    gemm_ms = max_over_ranks(gemm_ms_rank)
+    exch_ms = 0.0
+    if G > 1:
+        A0 = torch.empty((0, n), dtype=torch.float64, device=dev)
+        C0 = torch.empty((0, p), dtype=torch.float64, device=dev)
+        exch_ms, _ = timed(lambda: moa.gemm_lifted(0, A0, B, C0, comm), 3)
+        exch_ms /= 3
+    step_ms = elapsed_ms / args.steps
     kflops = 2.0 * rows * n * p
-    achieved_tf = kflops / (kern_ms / 1e3) / 1e12
+    achieved_tf = kflops / (gemm_ms_rank / 1e3) / 1e12 if rows else 0.0
+    achieved_tf = max_over_ranks(-achieved_tf) * -1 if G > 1 else achieved_tf  # the slowest rank's kernel
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_k1_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(str(N))
+            traffic = json.load(open(prof)).get(f"{rows}x{n}x{p}")
         except Exception:
             traffic = None
     plan = moa.plan(rows, n, p)
+    if exchange == "pull" and G > 1 and rank != 0:
+        launches = len(moa.pull_panels(n)) - 1
+    elif exchange == "nccl" and G > 1:
+        launches = moa.lift_panels(n, p, moa.F64, G)
+    else:
+        launches = 1
+    launches = int(max_over_ranks(launches))
 
     # energy (NVML; J per GEMM step summed over every participating GPU)
     energy = None
-    if ws > 1:
-        t = torch.tensor([float((e1 - e0) if (e0 is not None and e1 is not None) else -1e30)], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        e0, e1 = (0.0, float(t.item())) if t.item() >= 0 else (None, None)
-    if e0 is not None and e1 is not None:
-        j = (e1 - e0) / 1e3
-        idle_j = (idle_w or 0.0) * ws * (elapsed_ms / 1e3)
-        energy = {"j_per_gemm": round(j / args.steps, 4), "idle_w": idle_w,
-                  "j_per_gemm_above_idle": round((j - idle_j) / args.steps, 4) if idle_w is not None else None,
-                  "window_s": round(elapsed_ms / 1e3, 3),
-                  "avg_w": round(j / (elapsed_ms / 1e3), 1), "gflops_per_w": round(value / (j / (elapsed_ms / 1e3)), 2)}
+    ej = sum_over_ranks((e1 - e0) / 1e3 if (e0 is not None and e1 is not None) else -1e30)
+    if ej >= 0:
+        idle_j = (idle_w_sum or 0.0) * (elapsed_ms / 1e3)
+        energy = {"j_per_gemm": round(ej / args.steps, 3), "idle_w_all_gpus": idle_w_sum,
+                  "j_per_gemm_above_idle": round((ej - idle_j) / args.steps, 3) if idle_w_sum is not None else None,
+                  "window_s": round(elapsed_ms / 1e3, 3), "avg_w_all_gpus": round(ej / (elapsed_ms / 1e3), 1),
+                  "gflops_per_w": round(value / (ej / (elapsed_ms / 1e3)), 2)}
 
-    # e2e through moa_gemm_host (host buffers, copies inside the timed region)
+    # the other exchange, measured beside the headline (G > 1)
+    variants = None
+    if G > 1 and not args.no_variants:
+        variants = {exchange: {"ms_per_step": round(step_ms, 3), "gflops": round(value, 1)}}
+        other = "nccl" if exchange == "pull" else "pull"
+        try:
+            B_hold["other"] = make_B(other)
+            Bo = B_hold["other"]
+            step(Bo)
+            torch.cuda.synchronize()
+            k2 = max(2, min(args.steps, 5))
+            el2, _ = timed(lambda: step(Bo), k2)
+            variants[other] = {"ms_per_step": round(el2 / k2, 3), "gflops": round(flops_step * k2 / (el2 / 1e3) / 1e9, 1)}
+            if other == "pull":
+                torch.cuda.synchronize()
+                dist.barrier()
+                comm.free_window(Bo)
+            B_hold.clear()
+        except Exception as e:  # report, keep the headline
+            variants[other] = {"error": f"{type(e).__name__}: {e}"[:300]}
+
+    # e2e through the public host-buffer API (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
         hA = torch.empty((rows, n), dtype=torch.float64).pin_memory()
-        hB = torch.empty((n, p), dtype=torch.float64).pin_memory()
         hC = torch.empty((rows, p), dtype=torch.float64).pin_memory()
         hA.copy_(A.cpu())
-        hB.copy_(B.cpu())
-        k_e2e = max(1, min(args.steps, 5))
-        if ws > 1:
-            dist.barrier()
+        hB = None
+        if rank == 0:
+            hB = torch.empty((n, p), dtype=torch.float64).pin_memory()
+            hB.copy_(B.cpu())
+        Bd = B  # (a window when the exchange is pulled: a valid NCCL buffer for the host path's broadcasts)
 
         def e2e_step():
-            if comm is None:
-                moa.gemm_host(hA, hB, hC, A, B, C)
+            if G == 1:
+                moa.gemm_host(hA, hB, hC, A, Bd, C)
             else:
-                moa.gemm_lifted_host(m_total, hA, hB if rank == 0 else None, hC, A, B, C, comm)
+                moa.gemm_lifted_host(m, hA, hB, hC, A, Bd, C, comm)
         e2e_step()
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(k_e2e):
-            e2e_step()
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = a.elapsed_time(b)
-        if ws > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        h2d = (rows * n + (n * p if rank == 0 or ws == 1 else 0)) * 8
+        k_e2e = max(1, min(args.steps, 3))
+        e2e_ms, _ = timed(e2e_step, k_e2e)
+        h2d = int(sum_over_ranks((rows * n + (n * p if rank == 0 else 0)) * 8))
+        d2h = int(sum_over_ranks(rows * p * 8))
         e2e = {"value": round(flops_step * k_e2e / (e2e_ms / 1e3) / 1e9, 2), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": rows * p * 8, "steps": k_e2e,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": k_e2e,
                "ms_per_step": round(e2e_ms / k_e2e, 3),
-               "api": "moa_gemm_host" if comm is None else "moa_gemm_lifted_host"}
+               "api": "moa_gemm_host" if G == 1 else "moa_gemm_lifted_host (B via NCCL panels)"}
+        del hA, hB, hC
 
-    # N sweep (GFLOP/s and J/GEMM vs N), rank 0 at N = 1 only
+    free_B(B)
+    del A, B, C
+
+    # N sweep (GFLOP/s and J/GEMM vs N, the paper's study), G = 1 only
     sweep = None
-    if ws == 1 and not args.no_sweep:
-        sweep = []
+    if G == 1 and not args.no_sweep:
+        torch.cuda.empty_cache()
+        idle_s = sampler.idle_watts(2.0)
+        pts, points = [], []
         for Ns in [int(x) for x in args.sweep_sizes.split(",") if x]:
             As = torch.empty((Ns, Ns), dtype=torch.float64, device=dev)
             Bs = torch.empty((Ns, Ns), dtype=torch.float64, device=dev)
@@ -458,22 +575,32 @@ def main():
             for _ in range(3):
                 moa.gemm(As, Bs, out=Cs)
             torch.cuda.synchronize()
-            est = 2.0 * Ns ** 3 / (FP64_DMMA_PEAK_TFLOPS * 0.8e12)
-            reps = max(5, int(1.0 / est))  # >= ~1 s window for NVML energy granularity
+            est = 2.0 * Ns ** 3 / (FP64_DMMA_PEAK_TFLOPS * 0.9e12)
+            reps = max(3, math.ceil(1.05 / est))  # each window >= 1 s (NVML energy granularity)
+            wins = []
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0 = sampler.energy_mj()
-            a.record(stream)
-            for _ in range(reps):
-                moa.gemm(As, Bs, out=Cs)
-            b.record(stream)
-            torch.cuda.synchronize()
-            s1 = sampler.energy_mj()
-            ms = a.elapsed_time(b) / reps
+            for _ in range(args.sweep_windows):
+                s0 = sampler.energy_mj()
+                a.record(stream)
+                for _ in range(reps):
+                    moa.gemm(As, Bs, out=Cs)
+                b.record(stream)
+                torch.cuda.synchronize()
+                s1 = sampler.energy_mj()
+                ms = a.elapsed_time(b)
+                wins.append((ms / reps, (s1 - s0) / 1e3 / reps if s0 is not None else None, ms / 1e3))
+            ms = statistics.median(w[0] for w in wins)
             rec = {"N": Ns, "ms": round(ms, 4), "gflops": round(2.0 * Ns ** 3 / (ms / 1e3) / 1e9, 1),
-                   "frac_of_peak": round(2.0 * Ns ** 3 / (ms / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS, 4), "reps": reps,
+                   "frac_of_peak": round(2.0 * Ns ** 3 / (ms / 1e3) / 1e12 / FP64_DMMA_PEAK_TFLOPS, 4),
+                   "reps_per_window": reps, "windows": len(wins), "window_s": round(min(w[2] for w in wins), 3),
                    "l2": "warm (back-to-back launches)" if 3 * 8 * Ns * Ns < 126e6 else "inputs larger than L2"}
-            if s0 is not None and s1 is not None:
-                rec["j_per_gemm"] = round((s1 - s0) / 1e3 / reps, 5)
+            if wins[0][1] is not None:
+                js = sorted(w[1] for w in wins)
+                rec["j_per_gemm"] = round(statistics.median(js), 5)
+                rec["j_per_gemm_spread"] = [round(js[0], 5), round(js[-1], 5)]
+                if idle_s is not None:
+                    rec["j_per_gemm_above_idle"] = round(statistics.median(js) - idle_s * ms / 1e3, 5)
+                pts.append((Ns, rec["j_per_gemm"], rec.get("j_per_gemm_above_idle")))
             if 3 * 8 * Ns * Ns < 126e6:
                 # cold variant: a 256 MiB write flushes L2 before each launch;
                 # events bracket the GEMM alone
@@ -488,50 +615,55 @@ def main():
                     cold.append(a.elapsed_time(b))
                 del flush
                 rec["cold_l2_ms"] = round(statistics.median(cold), 4)
-            sweep.append(rec)
+            points.append(rec)
             del As, Bs, Cs
-        pts = [(r["N"], r.get("j_per_gemm")) for r in sweep if r.get("j_per_gemm")]
+            torch.cuda.empty_cache()
+        sweep = {"points": points, "idle_w": idle_s, "windows_per_size": args.sweep_windows,
+                 "paper_claim": "energy quadratic in N, i.e. linear in the size of matrix (P:14-15)"}
         if len(pts) >= 3:
-            import math
-            xs = [math.log(x) for x, _ in pts]
-            ys = [math.log(y) for _, y in pts]
-            mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
-            slope = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs)
-            sweep = {"points": sweep, "energy_exponent_fit": round(slope, 3),
-                     "paper_claim": "energy quadratic in N (P:14-15)"}
-        else:
-            sweep = {"points": sweep}
+            sweep["energy_exponent_fit"] = round(_fit_exponent([(x, y) for x, y, _ in pts]), 3)
+            if all(z and z > 0 for _, _, z in pts):
+                sweep["energy_exponent_fit_above_idle"] = round(_fit_exponent([(x, z) for x, _, z in pts]), 3)
+            sweep["fit_range"] = [pts[0][0], pts[-1][0]]
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_oracle_sample(m_total, n, p)
+    if rank == 0 and G == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(m, n, p)
 
-    if comm is not None:
-        comm.close()
-    if lifted:
-        dist.destroy_process_group()
+    comm.close()
+    dist.destroy_process_group()
     if rank != 0:
         return 0
-    cfg = workload_config(N, ws, lifted, args.gather)
-    cfg["plan"] = {"kernel": plan.kernel, "bm": plan.bm, "bn": plan.bn, "bk": plan.bk, "stages": plan.stages,
-                   "grid": plan.grid, "tiles": plan.tiles}
+    cfg = workload_config(N, G, exchange)
+    cfg["plan_rank0"] = {"kernel": plan.kernel, "bm": plan.bm, "bn": plan.bn, "bk": plan.bk, "stages": plan.stages,
+                         "grid": plan.grid, "tiles": plan.tiles}
+    if fallback:
+        cfg["exchange_fallback"] = fallback
+    sm = clocks.get("sm_mhz")
     line = {
         "metric": METRIC, "value": round(value, 2),
-        "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "unit": "GFLOP/s", "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": cfg,
         "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": round(achieved_tf / FP64_DMMA_PEAK_TFLOPS, 4),
-                     "traffic": traffic, "kernel": "k_dgemm_tma (fp64 DMMA)", "kernel_ms": round(kern_ms, 4),
-                     "algorithmic_flops_per_launch": kflops, "peak_source": FP64_PEAK_SOURCE},
-        "components": {"step_ms": round(elapsed_ms / args.steps, 4), "gemm_ms": round(kern_ms, 4),
-                       "exchange_ms": round(max(0.0, elapsed_ms / args.steps - kern_ms), 4)},
+                     "traffic": traffic, "kernel": "k_dgemm_tma (fp64 DMMA) on one rank's rows",
+                     "kernel_ms": round(gemm_ms, 3), "algorithmic_flops_per_launch": kflops,
+                     "peak_source": FP64_PEAK_SOURCE,
+                     "nominal_at_clock": round(148 * 64 * 2 * sm / 1e6, 2) if sm else None,
+                     "frac_of_nominal_at_clock": round(achieved_tf / (148 * 64 * 2 * sm / 1e6), 4) if sm else None},
+        "components": {"step_ms": round(step_ms, 3), "compute_ms": round(gemm_ms, 3),
+                       "exchange_alone_ms": round(exch_ms, 3),
+                       "exposed_exchange_ms": round(max(0.0, step_ms - gemm_ms), 3), "gather_ms": 0.0,
+                       "step_ms_min_median_max": [round(min(per_step), 3), round(statistics.median(per_step), 3),
+                                                  round(max(per_step), 3)]},
+        "exchange_variants": variants,
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": launches * args.steps,
         "energy": energy,
         "sweep": sweep,
-        "clocks": sampler.summary(),
+        "clocks": clocks,
         "cpu_baseline": cpu,
     }
     emit(line)

@@ -29,7 +29,8 @@ def test_reference_arm_prints_one_json_line():
     assert KEYS <= set(d), KEYS - set(d)
     assert d["impl"] == "reference" and d["unit"] == "GFLOP/s" and d["higher_is_better"] is True
     assert d["steps"] == 2 and d["warmup"] == 1 and d["value"] > 0
-    assert d["config"]["n"] == 64 and d["config"]["workload"].startswith("square fp64 GEMM")
+    assert d["config"]["n"] == 64 and "BASELINE configs[4]" in d["config"]["workload"]
+    assert d["scaling"] == "strong" and d["config"]["rows_per_rank"] == [64]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
 
 
@@ -50,3 +51,26 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = _run(["--impl", "reference", "--N", "32", "--steps", "1", "--warmup", "0"],
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0 and r.stdout.strip() == "", r.stdout
+
+
+def test_gpus_without_enough_devices_fails_loudly():
+    """bench.py --gpus 2 (no torchrun) launches its 2 ranks itself — or, with fewer
+    visible GPUs (here: none), exits non-zero with a clear message instead of silently
+    measuring one GPU (round-1 review)."""
+    r = _run(["--gpus", "2", "--steps", "1", "--warmup", "0"])
+    assert r.returncode != 0
+    assert "needs 2 visible GPUs" in r.stderr, r.stderr[-2000:]
+    assert r.stdout.strip() == ""
+
+
+def test_world_size_must_match_gpus():
+    r = _run(["--gpus", "4", "--steps", "1", "--warmup", "0"], env={"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr, r.stderr[-2000:]
+
+
+def test_reference_arm_config_matches_gpu_arm_for_each_G():
+    import bench
+    for G in (1, 2, 4, 8):
+        cfg = bench.workload_config(32768, G)
+        assert cfg["m"] == cfg["n"] == cfg["p"] == 32768
+        assert sum(cfg["rows_per_rank"]) == 32768 and len(cfg["rows_per_rank"]) == G

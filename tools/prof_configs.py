@@ -6,7 +6,7 @@ it with -s 1 and captures the second.
     python tools/prof_configs.py <config>
 configs: c0 (fp64 256^3), c3 (fp64 65536x512x512), c16k (fp64 16384^3),
          f32 (exact fp32 16384^3), tf32 (3xTF32 16384^3), had (Hadamard fp64 16384^2),
-         kron (Kronecker fp64 128^2 x 128^2)
+         kron (Kronecker fp64 128^2 x 128^2), l1/l2/l4/l8 (rank 0's rows of configs[4] at G)
 """
 import os
 import sys
@@ -21,7 +21,10 @@ from inputs import inputs as I  # noqa: E402
 SHAPES = {"c0": (256, 256, 256, torch.float64), "c3": (65536, 512, 512, torch.float64),
           "c16k": (16384, 16384, 16384, torch.float64), "f32": (16384, 16384, 16384, torch.float32),
           "tf32": (16384, 16384, 16384, torch.float32), "had": (16384, 16384, 0, torch.float64),
-          "kron": (128, 128, 128, torch.float64)}
+          "kron": (128, 128, 128, torch.float64),
+          # BASELINE configs[4]: rank 0's rows of the row-lifted 32768^3 at G = 1, 2, 4, 8
+          "l1": (32768, 32768, 32768, torch.float64), "l2": (16384, 32768, 32768, torch.float64),
+          "l4": (8192, 32768, 32768, torch.float64), "l8": (4096, 32768, 32768, torch.float64)}
 
 
 def main(cfg):
