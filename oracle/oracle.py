@@ -24,7 +24,9 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# MOA_ORACLE_LIBRARY: an instrumented build of the same source (tests/test_sanitizers.py
+# loads oracle/liboracle_asan.so, -fsanitize=address,undefined); default: liboracle.so
+_LIB_PATH = os.environ.get("MOA_ORACLE_LIBRARY") or os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 _i64 = ctypes.c_int64

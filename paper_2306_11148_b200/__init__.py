@@ -32,7 +32,10 @@ KERNEL_NAMES = {0: "none", 1: "zero_fill", 2: "dgemm_tma", 3: "dgemm_generic", 4
                 6: "sgemm_generic"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libmoa.so")
+# MOA_LIBRARY: an instrumented build of the same sources (tests/test_sanitizers.py loads
+# build/asan/libmoa_asan.so, host code under -fsanitize=address,undefined); default: the
+# in-tree libmoa.so. Never a different implementation.
+lib_path = os.environ.get("MOA_LIBRARY") or os.path.join(_HERE, "libmoa.so")
 
 if not os.path.exists(lib_path):
     raise ImportError(

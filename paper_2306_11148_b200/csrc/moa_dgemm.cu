@@ -196,6 +196,28 @@ __device__ __forceinline__ void store_acc(const Acc<MA, NBOX>& c, double* __rest
   }
 }
 
+#ifdef MOA_K1_PHASES
+// PHASE-BREAKDOWN EXPERIMENT (variant builds with -DMOA_K1_PHASES only; the product
+// never defines it): per CTA, %globaltimer (ns) at kernel entry, after
+// griddepcontrol.wait, at the producer's first TMA issue, and for consumer warp 0 /
+// lane 0 the first slab's landing, the summed full-barrier waits, the end of the last
+// slab and the end of the store. Read back with moa_k1_phases_read (tools/experiments/phases.py).
+__device__ unsigned long long g_ph[1024 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MOA_PH(slot, v) \
+  do {                 \
+    if (blockIdx.x < 1024) g_ph[blockIdx.x * 8 + (slot)] = (v); \
+  } while (0)
+#else
+#define MOA_PH(slot, v) \
+  do {                 \
+  } while (0)
+#endif
+
 // ------------------------------- K1: TMA + WS --------------------------------
 // Register file is split per SM sub-partition (warp w -> SMSP w % 4, 16384
 // registers each). With 8 consumer warps a lone producer warp would put 3 warps
@@ -221,7 +243,7 @@ struct K1Traits {
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 24 * STAGES;  // + piece descriptors
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 32 * STAGES;  // + piece descriptors
   static_assert(BM == 8 * kMA * WARPS_M && (kMA == 1 || kMA == 2 || kMA == 4), "warp tile is 8, 16 or 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -235,10 +257,25 @@ template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
                                               int& stage, uint32_t& phase, double* __restrict__ C, int64_t m,
                                               int64_t p, int64_t ldc, int64_t row0, int64_t col0, int wm, int wn,
-                                              int k0, int k1, bool load, const FragOffsets& f, int lane) {
+                                              int k0, int k1, bool load, const FragOffsets& f, int lane,
+                                              bool release) {
   load_acc<MA, NBOX, true>(acc, C, load ? m : 0, p, ldc, row0 + wm * 8 * MA, col0 + wn * NBOX * 16, f);
+#ifdef MOA_K1_PHASES
+  unsigned long long waited = 0, tw0 = 0;
+  const bool ph = threadIdx.x == 0;
+#endif
   for (int kt = k0; kt < k1; ++kt) {
+#ifdef MOA_K1_PHASES
+    if (ph) tw0 = gtime();
+#endif
     mbar_wait(full0 + 8 * stage, phase);  // (ptxas reconverges the spin with BSSY/BSYNC before the DMMAs)
+#ifdef MOA_K1_PHASES
+    if (ph) {
+      const unsigned long long tw1 = gtime();
+      waited += tw1 - tw0;
+      if (kt == k0) MOA_PH(3, tw1);
+    }
+#endif
     const uint8_t* sa = sptr + stage * STAGE_BYTES;
     mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
     // WAR across proxies: these generic-proxy LDS reads must be ordered before the
@@ -246,15 +283,28 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
     // alone does not do it (ptxas even hoists the arrive above the slab's last
     // DMMAs): without this fence whole warp tiles were computed from overwritten
     // operands, rarely under dynamic scheduling, often under stream-K.
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    // A one-shot launch (one tile per CTA, all of k resident: no stage is ever
+    // refilled) skips the release entirely.
+    if (release) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+    }
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1u;
     }
   }
+#ifdef MOA_K1_PHASES
+  if (ph) {
+    MOA_PH(4, waited);
+    MOA_PH(5, gtime());
+  }
+#endif
   store_acc<MA, NBOX, true>(acc, C, m, p, ldc, row0 + wm * 8 * MA, col0 + wn * NBOX * 16, f);
+#ifdef MOA_K1_PHASES
+  if (ph) MOA_PH(6, gtime());
+#endif
 }
 
 // ACC: start every tile's chain from the C in memory (moa_gemm_acc k-panel chains).
@@ -269,12 +319,18 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
 //  * tile_ctr == null, flags != null: every tile is in the stream-K region
 //    (tiles < 2G): run r = CTA index.
 //  * neither: static stride (tiles <= grid).
-// The producer publishes each piece (tile, k0, k1, run) in the slot of its first
-// stage, before that stage's full-barrier arrive (release); t = -1 ends the work.
+// The producer publishes each piece (tile coordinates, k0, k1, run) in the slot of
+// its first stage with st.async, whose bytes complete on that stage's full barrier
+// like the TMA loads: a consumer that waited on the stage reads a complete
+// descriptor, and every write of the slot is in the async proxy (ordered after the
+// consumers' reads of the previous use by their fence.proxy.async before the empty
+// arrive). tm = -1 ends the work. (A generic st.shared handoff ordered by the
+// mbarrier's release/acquire was correct too, but compute-sanitizer racecheck does
+// not model mbarriers and reported it.)
 struct PieceDesc {
-  int64_t t;
-  int32_t k0, k1, run, pad;
+  int32_t tm, tn, k0, k1, run, pad[3];
 };
+constexpr uint32_t kDescBytes = 20;  // tm, tn, k0, k1 (v4) + run
 
 //
 // PEER: the fused GEMM -> all-gather epilogue (moa_gemm_lifted_gather). Every FINAL
@@ -288,7 +344,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ flags,
-                unsigned int* __restrict__ tile_ctr, const __grid_constant__ PeerDst peers) {
+                unsigned int* __restrict__ tile_ctr, const __grid_constant__ PeerDst peers, int oneshot) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -296,9 +352,13 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
-  volatile PieceDesc* desc = reinterpret_cast<volatile PieceDesc*>(smem_raw + (empty0 + STAGES * 8 - raw));
+  const uint32_t desc0 = empty0 + STAGES * 8;  // 16-B aligned (v4 st.async)
+  volatile PieceDesc* desc = reinterpret_cast<volatile PieceDesc*>(smem_raw + (desc0 - raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (int)((n + kBK - 1) / kBK);
+#ifdef MOA_K1_PHASES
+  if (threadIdx.x == 0) MOA_PH(0, gtime());
+#endif
 
   // Programmatic dependent launch: this prologue may run while the previous grid in
   // the stream drains; griddepcontrol.wait (below) orders every global-memory access
@@ -316,6 +376,9 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   }
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef MOA_K1_PHASES
+  if (threadIdx.x == 0) MOA_PH(1, gtime());
+#endif
 
   if (warp >= Tr::kConsumerWarps) {
     // ----------------------------- producer ---------------------------------
@@ -331,14 +394,18 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
         const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
         for (int kt = k0; kt < k1; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1u);
-          if (kt == k0) {
-            desc[stage].t = t;
-            desc[stage].k0 = k0;
-            desc[stage].k1 = k1;
-            desc[stage].run = run;
-          }
           const uint32_t fb = full0 + 8 * stage;
-          mbar_arrive_expect_tx(fb, Tr::kStageBytes);
+#ifdef MOA_K1_PHASES
+          if (kt == 0) MOA_PH(2, gtime());
+#endif
+          if (kt == k0) {
+            mbar_arrive_expect_tx(fb, Tr::kStageBytes + kDescBytes);
+            const uint32_t d = desc0 + 32 * stage;
+            st_async_v4(d, (int32_t)tm, (int32_t)tn, k0, k1, fb);
+            st_async_b32(d + 16, run, fb);
+          } else {
+            mbar_arrive_expect_tx(fb, Tr::kStageBytes);
+          }
           const uint32_t sa = sbase + stage * Tr::kStageBytes;
           tma_load_2d(sa, &tmA, fb, kt * kBK, row0);
 #pragma unroll
@@ -376,12 +443,18 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
           }
           break;
         }
+      } else if (oneshot) {
+        // one tile per CTA with all of k resident (ktiles <= STAGES, grid == tiles):
+        // every TMA is issued at once, no stage is reused, no end-of-work sentinel
+        emit(blockIdx.x, 0, ktiles, -1);
       } else {
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) emit(t, 0, ktiles, -1);
       }
-      mbar_wait(empty0 + 8 * stage, phase ^ 1u);  // end-of-work sentinel slot
-      desc[stage].t = -1;
-      mbar_arrive(full0 + 8 * stage);
+      if (!oneshot) {
+        mbar_wait(empty0 + 8 * stage, phase ^ 1u);  // end-of-work sentinel slot
+        mbar_arrive_expect_tx(full0 + 8 * stage, 16);
+        st_async_v4(desc0 + 32 * stage, -1, 0, 0, 0, full0 + 8 * stage);
+      }
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
@@ -404,16 +477,15 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     // (consume_piece waits on the same, already complete, phase again).
     mbar_wait(full0 + 8 * stage, phase);
     __syncwarp();
-    const int64_t t = desc[stage].t;
-    if (t < 0) break;
+    const int64_t tm = desc[stage].tm;
+    if (tm < 0) break;
+    const int64_t tn = desc[stage].tn;
     const int k0 = desc[stage].k0, k1 = desc[stage].k1, run = desc[stage].run;
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
-    int64_t tm, tn;
-    tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(acc, sptr, full0, empty0, stage, phase, C, m, p,
                                                                    ldc, tm * BM, tn * BN, wm, wn, k0, k1,
-                                                                   ACC || tail, f, lane);
+                                                                   ACC || tail, f, lane, !oneshot);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
     if constexpr (PEER) {
@@ -422,6 +494,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
           store_acc<Tr::kMA, Tr::kNBox, true>(acc, reinterpret_cast<double*>(peers.dst[d]), m, p, ldc,
                                               tm * BM + wm * 8 * Tr::kMA, tn * BN + wn * Tr::kNBox * 16, f);
     }
+    if (oneshot) break;
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -540,8 +613,10 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // one tile per CTA and all of k resident in the ring: no stage is ever refilled
+  const int oneshot = (plan.tiles <= plan.grid && (n + kBK - 1) / kBK <= ST) ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                     (int)plan.raster_group, flags, ctr, peers);
+                                     (int)plan.raster_group, flags, ctr, peers, oneshot);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -567,7 +642,10 @@ TileConfig kK1Configs[] = {
     {MOA_KERNEL_DGEMM_TMA, 64, 32, 16, 4, K1Traits<64, 32, 2, 2, 4>::kThreads, 4, K1Traits<64, 32, 2, 2, 4>::kSmem, 0.0},
     // latency tiles (16x16 outputs per warp): eta here is the latency-regime factor;
     // the chooser considers them only for tiny problems (moa_host.cpp choose()).
-    // 16x32 first: it wins the ties (N=512: 13.2 vs 22.3 us for 16x16).
+    // 16x32 first: it wins the ties (N=512: 13.2 vs 22.3 us for 16x16). Its one-shot
+    // form (16 stages = all of k <= 256 resident, one tile per CTA) goes first of all:
+    // every TMA is in flight at once and no slab pays a release (fence + arrive).
+    {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 16, K1Traits<16, 32, 1, 2, 16>::kThreads, 2, K1Traits<16, 32, 1, 2, 16>::kSmem, 1.0, 16},
     {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 4, K1Traits<16, 32, 1, 2, 4>::kThreads, 8, K1Traits<16, 32, 1, 2, 4>::kSmem, 1.0},
     {MOA_KERNEL_DGEMM_TMA, 16, 16, 16, 4, K1Traits<16, 16, 1, 1, 4>::kThreads, 8, K1Traits<16, 16, 1, 1, 4>::kSmem, 1.0},
 };
@@ -589,9 +667,10 @@ void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
     RelaxedCapture relaxed_capture;
-    int o[6] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
-                k1_occupancy<64, 32, 2, 2, 4>(), k1_occupancy<16, 32, 1, 2, 4>(), k1_occupancy<16, 16, 1, 1, 4>()};
-    for (int i = 0; i < 6; ++i)
+    int o[7] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
+                k1_occupancy<64, 32, 2, 2, 4>(),   k1_occupancy<16, 32, 1, 2, 16>(), k1_occupancy<16, 32, 1, 2, 4>(),
+                k1_occupancy<16, 16, 1, 1, 4>()};
+    for (int i = 0; i < 7; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
@@ -621,6 +700,7 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
   if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 2, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 4, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 32 && plan.stages == 4) return launch_k1<64, 32, 2, 2, 4>(plan, g, stream);
+  if (plan.bm == 16 && plan.bn == 32 && plan.stages == 16) return launch_k1<16, 32, 1, 2, 16>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 32 && plan.stages == 4) return launch_k1<16, 32, 1, 2, 4>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 16 && plan.stages == 4) return launch_k1<16, 16, 1, 1, 4>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
@@ -642,3 +722,14 @@ int launch_dgemm_generic(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t
 }
 
 }  // namespace moa
+
+#ifdef MOA_K1_PHASES
+extern "C" int moa_k1_phases_read(unsigned long long* host, int n) {
+  if (n > 1024 * 8) n = 1024 * 8;
+  return (int)cudaMemcpyFromSymbol(host, moa::g_ph, sizeof(unsigned long long) * (size_t)n);
+}
+extern "C" int moa_k1_phases_clear() {
+  static unsigned long long z[1024 * 8] = {};
+  return (int)cudaMemcpyToSymbol(moa::g_ph, z, sizeof(z));
+}
+#endif

@@ -252,6 +252,10 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
   for (int i = 0; i < nc; ++i) {
     const TileConfig& c = cfgs[i];
     if (c.smem_bytes > ds.smem_optin) continue;
+    if (c.max_ktiles > 0) {  // one-shot: all of k resident, one resident CTA per tile
+      const int64_t tl = ((m + c.bm - 1) / c.bm) * ((p + c.bn - 1) / c.bn);
+      if ((n + c.bk - 1) / c.bk > c.max_ktiles || tl > (int64_t)ds.sms * c.ctas_per_sm) continue;
+    }
     double eta = c.eta;
     if (eta <= 0.0) {
       // A 32-column tile (K1 64x32) is offered only where every 64-column tile would

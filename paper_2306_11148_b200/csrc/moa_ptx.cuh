@@ -50,6 +50,19 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// Asynchronous (async-proxy) stores into this CTA's shared memory that complete
+// transaction bytes on an mbarrier, like a TMA load: the piece descriptors of K1/K3
+// travel with the stage they describe, so a consumer that has waited on the stage's
+// full barrier sees them, and no generic-proxy store races with its reads.
+__device__ __forceinline__ void st_async_v4(uint32_t dst, int32_t a, int32_t b, int32_t c, int32_t d, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_b32(uint32_t dst, int32_t a, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst), "r"(a), "r"(bar)
+               : "memory");
+}
 // Order this thread's generic-proxy shared-memory accesses with later async-proxy
 // (TMA / tensor-core) accesses of the same bytes. Needed by every consumer that
 // reads a stage with ld.shared before releasing it to a TMA producer (WAR), and

@@ -146,7 +146,7 @@ int main(void) {
     libdir = os.path.dirname(moa.lib_path)
     exe = tmp_path / "abi_user"
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
-                        "-o", str(exe), "-L", libdir, "-l:libmoa.so", "-Wl,-rpath," + libdir],
+                        "-o", str(exe), "-L", libdir, "-l:" + os.path.basename(moa.lib_path), "-Wl,-rpath," + libdir],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)

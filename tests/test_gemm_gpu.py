@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 # every compiled K1 tile config (bm, bn, stages), incl. the latency tiles
-K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
+K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 16), (16, 32, 4), (16, 16, 4)]
 
 
 def _moa():
@@ -183,6 +183,27 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
         moa.gemm_with_plan(tA, tB, out, pl)
         torch.cuda.synchronize()
         assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 256), (250, 256, 250), (1, 16, 2), (17, 254, 34), (160, 96, 480),
+                                   (300, 200, 260)])
+def test_oneshot_latency_tiles_bitwise(cuda_device, shape):
+    """Tiny problems (configs[0], 256^3): the chooser's one-shot 16x32 latency tile
+    (all of k resident in a 16-stage ring, one tile per CTA, no stage release) gives
+    the fused ip.c bits, ragged edges included; the literal ip.c within 1e-12 sqrt(n)."""
+    import torch
+    moa = _moa()
+    m, n, p = shape
+    A, B = _host(m, n, p, 31)
+    pl = moa.plan(m, n, p)
+    assert (pl.bm, pl.bn, pl.stages) == (16, 32, 16), pl
+    assert pl.grid == pl.tiles
+    out = moa.gemm(torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device))
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert _bits_equal(got, O.ip(A, B, fused=True))
+    lit = O.ip(A, B, fused=False)
+    assert np.linalg.norm(got - lit) <= 1e-12 * np.sqrt(n) * np.linalg.norm(lit)
 
 
 @pytest.mark.parametrize("shape", [(2000, 200, 2000), (1500, 100, 3000), (2100, 56, 1030)])

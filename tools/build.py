@@ -123,8 +123,41 @@ def build_shim(force=False):
     return out
 
 
+def build_asan(force=False):
+    """Sanitizer builds of the HOST code (tests/test_sanitizers.py): the oracle, and
+    libmoa.so with moa_host.cpp / moa_tma.cpp compiled by g++ -fsanitize=address,undefined
+    (the device translation units are the product's own objects, build/moa/*.cu.o)."""
+    build_moa(force)
+    nccl = _nccl_root()
+    san = ["-fsanitize=address,undefined", "-fno-sanitize-recover=all", "-fno-omit-frame-pointer", "-g", "-O1"]
+    src = os.path.join(ROOT, "oracle", "moa_oracle.c")
+    out_o = os.path.join(ROOT, "oracle", "liboracle_asan.so")
+    if force or _stale(out_o, [src]):
+        _run(["gcc", *san, "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-shared", "-pthread", src, "-o",
+              out_o, "-lm"])
+    csrc = os.path.join(ROOT, "paper_2306_11148_b200", "csrc")
+    objdir = os.path.join(ROOT, "build", "asan")
+    os.makedirs(objdir, exist_ok=True)
+    host = [os.path.join(csrc, "moa_host.cpp"), os.path.join(csrc, "moa_tma.cpp")]
+    hdrs = sorted(glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh"))
+                  + glob.glob(os.path.join(ROOT, "include", "*.h")))
+    out = os.path.join(objdir, "libmoa_asan.so")
+    dev_objs = sorted(glob.glob(os.path.join(ROOT, "build", "moa", "*.cu.o")))
+    if force or _stale(out, host + hdrs + dev_objs):
+        objs = []
+        for s in host:
+            o = os.path.join(objdir, os.path.basename(s) + ".o")
+            _run(["g++", *san, "-std=c++17", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", csrc, "-I",
+                  os.path.join(nccl, "include"), "-I", "/usr/local/cuda/include", "-c", s, "-o", o])
+            objs.append(o)
+        _run(["g++", *san, "-shared", *objs, *dev_objs, "-o", out, "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+              "-Wl,-rpath=" + os.path.join(nccl, "lib"), "-L/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath=/usr/local/cuda/lib64"])
+    return out
+
+
 TARGETS = {"oracle": build_oracle, "inputs": build_inputs, "inputs_cuda": build_inputs_cuda, "moa": build_moa,
-           "shim": build_shim}
+           "shim": build_shim, "asan": build_asan}
 
 
 def main(argv=None):
@@ -133,7 +166,7 @@ def main(argv=None):
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--ptxas-v", action="store_true")
     a = ap.parse_args(argv)
-    names = list(TARGETS) if "all" in a.targets else a.targets
+    names = [t for t in TARGETS if t != "asan"] if "all" in a.targets else a.targets
     for n in names:
         print(f"[build] {n}", flush=True)
         if n == "moa":

@@ -9,7 +9,7 @@ import paper_2306_11148_b200 as moa
 from inputs import inputs as I
 from oracle import oracle as O
 ok = True
-for (m, n, p) in [(200, 96, 260), (130, 34, 66)]:
+for (m, n, p) in [(200, 96, 260), (130, 34, 66), (256, 256, 256)]:
     for dt, prec in [(np.float64, None), (np.float32, None), (np.float32, "3xtf32")]:
         A = I.host_matrix(m, n, 2, I.ID_A, dtype=dt); B = I.host_matrix(n, p, 2, I.ID_B, dtype=dt)
         C = moa.gemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), precision=prec)

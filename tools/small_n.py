@@ -20,7 +20,7 @@ import paper_2306_11148_b200 as moa  # noqa: E402
 from inputs import inputs as I  # noqa: E402
 
 PEAK = 37.0
-CFGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
+CFGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 16), (16, 32, 4), (16, 16, 4)]
 
 
 def time_fn(fn, reps):
