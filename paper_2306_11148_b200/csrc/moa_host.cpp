@@ -6,6 +6,7 @@
 // citations). Readings R1..R16: DESIGN.md §Readings.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a profiler attaches
 
 #include <climits>
 #include <cstdint>
@@ -54,6 +55,16 @@ namespace moa {
 
 namespace {
 thread_local std::string g_last_error;
+
+// NVTX range around the host-side issue of one step of a lifted call (exchange,
+// compute, gather), so a profiler timeline (nsys / ncu --nvtx) attributes the
+// stream work each step enqueues.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 std::mutex g_dev_mu;
 std::map<int, DeviceShape> g_devs;
@@ -381,6 +392,7 @@ int run_plan(const moa_plan_t& plan, const GemmArgs& g, int dtype, cudaStream_t 
 // The common GEMM path: validate, plan (optionally honouring an explicit tile
 // choice), launch.
 int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t stream) {
+  Nvtx range("moa gemm");
   int rc = validate_g(g, dtype);
   if (rc) return rc;
   if (g.peers && g.peers->nd > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
@@ -1230,9 +1242,11 @@ static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const
   }
   cudaError_t e;
   int rc;
+  Nvtx whole("moa lifted rows");
   // phase 0: entry barrier
   for (const auto& o : ops)
     if (o.phase == 0 && (rc = issue_nccl(comm, o, nullptr, nullptr, dtype, s))) return rc;
+  Nvtx exch("moa exchange B");
   // phase 1: B's k-panels, on the side stream (when compute overlaps them) with one
   // event per panel, else on the compute stream
   bool has[kMaxPanels] = {};
@@ -1261,6 +1275,8 @@ static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const
       has[o.panel] = true;
     }
   }
+  nvtxRangePop();  // (end of "moa exchange B": its ops are enqueued)
+  nvtxRangePushA("moa lifted compute");
   // the lifted compute: this rank's rows of C, panel by panel. Panel j > 0 continues
   // every element's fma chain from panel j-1's C, so the result is bitwise the
   // one-launch result ("the addition loop to add up the blocks").
@@ -1274,6 +1290,8 @@ static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const
     if (j == K - 1) g.peers = last_peers;  // the final panel writes the final C
     if ((rc = gemm_reserving(g, dtype, s, reserve_sms && j < K - 1 ? kPipeCTAs : 0))) return rc;
   }
+  nvtxRangePop();
+  nvtxRangePushA("moa gather C / exit barrier");  // (popped by exch's destructor)
   // phase 2: gather of C (reading R14) / exit barrier
   int group = 0;
   for (size_t i = 0; i < ops.size(); ++i) {
