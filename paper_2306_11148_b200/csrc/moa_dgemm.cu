@@ -234,16 +234,30 @@ struct K1Traits {
   // warp) are meant to pack many CTAs per SM
   static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : (BM / WARPS_M <= 16 ? 8 : 2);
   static constexpr bool kSetMaxNReg = kProducerWarps == 4;
-  static constexpr int kProducerRegs = 40;
+  static constexpr int kProducerRegs = 40;  // 40 + 2 x 232 per SMSP; also the CTA pool: 4 x 40 + 8 x 232 = 12 x 168
   static constexpr int kConsumerRegs = 232;
   static constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
   static_assert(!kSetMaxNReg || (kProducerRegs + 2 * kConsumerRegs) * 32 <= 16384, "per-SMSP register budget");
+  // setmaxnreg moves registers inside the CTA's pool (every warp starts with the
+  // launch count, 65536 / threads rounded down to 8): a consumer .inc beyond what the
+  // producers' .dec released waits forever (a hang, not an error)
+  static_assert(!kSetMaxNReg || kProducerWarps * kProducerRegs + kConsumerWarps * kConsumerRegs <=
+                                    (kProducerWarps + kConsumerWarps) * ((65536 / ((kConsumerWarps + kProducerWarps) * 32)) & ~7),
+                "setmaxnreg: consumers ask for more registers than the producers release");
   static constexpr int kNBox = BN / WARPS_N / 16;
   static constexpr int kMA = BM / WARPS_M / 8;  // A atoms (8 rows each) per warp
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8 + 32 * STAGES;  // + piece descriptors
+  // Lagged consumer groups (8 consumer warps): warps 4..7 consume each stage only
+  // after warps 0..3 have (one lag barrier per stage), so the two warps of every SM
+  // sub-partition are a slab apart and never cross a tile boundary together.
+#ifdef MOA_K1_NO_LAG  // A/B variant builds only
+  static constexpr bool kLag = false;
+#else
+  static constexpr bool kLag = kConsumerWarps == 8;
+#endif
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 3 * STAGES * 8;  // + full/empty/lag barriers
   static_assert(BM == 8 * kMA * WARPS_M && (kMA == 1 || kMA == 2 || kMA == 4), "warp tile is 8, 16 or 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -253,12 +267,17 @@ struct K1Traits {
 // low-k partial of a split tile), else from +0: the loads are predicated off by
 // passing m = 0, so there is ONE copy of the slab loop in the kernel (a branch
 // between load_acc and acc_zero once cost 5.4% in register copies).
-template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
+// Lag (8 consumer warps, kLag): group 0 (warps 0..3) arrives on lag[stage] after its
+// slab; group 1 (warps 4..7) waits on it before its own. One warp of each group sits
+// on every SM sub-partition (SMSP = warp % 4), so while one group is at a tile
+// boundary (drain the DMMA chains, store C, read the next piece) the other still
+// has a slab of DMMAs for that SMSP's pipe.
+template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES, bool LAG>
 __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
-                                              int& stage, uint32_t& phase, double* __restrict__ C, int64_t m,
-                                              int64_t p, int64_t ldc, int64_t row0, int64_t col0, int wm, int wn,
-                                              int k0, int k1, bool load, const FragOffsets& f, int lane,
-                                              bool release) {
+                                              uint32_t lag0, int group, int& stage, uint32_t& phase,
+                                              double* __restrict__ C, int64_t m, int64_t p, int64_t ldc,
+                                              int64_t row0, int64_t col0, int wm, int wn, int k0, int k1, bool load,
+                                              const FragOffsets& f, int lane, bool release) {
   load_acc<MA, NBOX, true>(acc, C, load ? m : 0, p, ldc, row0 + wm * 8 * MA, col0 + wn * NBOX * 16, f);
 #ifdef MOA_K1_PHASES
   unsigned long long waited = 0, tw0 = 0;
@@ -269,6 +288,7 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
     if (ph) tw0 = gtime();
 #endif
     mbar_wait(full0 + 8 * stage, phase);  // (ptxas reconverges the spin with BSSY/BSYNC before the DMMAs)
+    if (LAG && group > 0) mbar_wait(lag0 + 8 * stage, phase);  // (group -1: this launch runs without lag)
 #ifdef MOA_K1_PHASES
     if (ph) {
       const unsigned long long tw1 = gtime();
@@ -278,6 +298,7 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
 #endif
     const uint8_t* sa = sptr + stage * STAGE_BYTES;
     mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
+    if (LAG && group == 0 && lane == 0) mbar_arrive(lag0 + 8 * stage);  // (no data: ordering of progress only)
     // WAR across proxies: these generic-proxy LDS reads must be ordered before the
     // producer's next TMA (async-proxy) write of this stage. The arrive's .release
     // alone does not do it (ptxas even hoists the arrive above the slab's last
@@ -309,28 +330,65 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
 
 // ACC: start every tile's chain from the C in memory (moa_gemm_acc k-panel chains).
 //
-// Work assignment (the producer decides; the consumers only read piece descriptors):
-//  * tile_ctr != null: whole tiles claimed dynamically from an atomic counter and,
-//    when flags != null (the last wave is partial), the stream-K runs of
-//    moa_ptx.cuh sk_run for the last S tiles, one run per CTA, claimed from the
-//    same counter. Claiming keeps all CTAs of a wave in k-lockstep, so they share
-//    the A/B k-slabs in L2 (a fully static schedule drifted: 53% L2 hits vs 82%
-//    at N=16384); the runs remove the partial last wave.
-//  * tile_ctr == null, flags != null: every tile is in the stream-K region
-//    (tiles < 2G): run r = CTA index.
-//  * neither: static stride (tiles <= grid).
-// The producer publishes each piece (tile coordinates, k0, k1, run) in the slot of
-// its first stage with st.async, whose bytes complete on that stage's full barrier
-// like the TMA loads: a consumer that waited on the stage reads a complete
-// descriptor, and every write of the slot is in the async proxy (ordered after the
-// consumers' reads of the previous use by their fence.proxy.async before the empty
-// arrive). tm = -1 ends the work. (A generic st.shared handoff ordered by the
-// mbarrier's release/acquire was correct too, but compute-sanitizer racecheck does
-// not model mbarriers and reported it.)
-struct PieceDesc {
-  int32_t tm, tn, k0, k1, run, pad[3];
+// Work assignment: every CTA walks its own static schedule (StaticSched: whole
+// tiles cta, cta + G, ... below the stream-K region, then its stream-K run r = cta),
+// computed identically by the producer and by every consumer warp, so nothing about
+// the schedule crosses shared memory (round 1 published piece descriptors with
+// plain shared stores ordered by the stage mbarrier: correct, but the one hazard
+// compute-sanitizer racecheck reported, since it does not model mbarriers). The
+// wave gate (producer) keeps the CTAs of a wave in k-lockstep, which round 1's
+// dynamic tile claiming only approximated.
+// launch mode bits (host -> K1)
+constexpr int kK1OneShot = 1;   // one tile per CTA, all of k resident: no stage release
+constexpr int kK1WaveGate = 2;  // wave gate (see the producer)
+constexpr int kK1Lag = 8;       // lagged consumer groups (8-warp tiles, shallow k)
+
+// One CTA's static schedule: whole tiles cta, cta + G, ... below
+// `first` (the stream-K region's start, or all tiles), then its stream-K run r = cta:
+// head first, whole run tiles, tail last (the order the hand-off argument of
+// moa_ptx.cuh needs).
+struct StaticSched {
+  // tile indices fit in 32 bits: C (>= 256 fp64 elements per tile) fits in HBM
+  int32_t t, first, G, w, hb, ta, f1;
+  int32_t hk, tk, ktiles, st;
+  __device__ __forceinline__ StaticSched(int64_t tiles, int ktiles_, int64_t G_, int64_t cta, bool sk)
+      : t((int32_t)cta), first((int32_t)(sk ? sk_first_tile(tiles, G_) : tiles)), G((int32_t)G_), w(0), hb(0),
+        ta(0), f1(0), hk(0), tk(0), ktiles(ktiles_), st(sk ? 0 : 3) {
+    if (sk) {
+      const SkRun q = sk_run(tiles, ktiles_, G_, cta);
+      hb = (int32_t)q.hb, ta = (int32_t)q.ta, w = (int32_t)q.f0, f1 = (int32_t)q.f1, hk = q.hk, tk = q.tk;
+    }
+  }
+  __device__ __forceinline__ bool next(int64_t& tile, int& k0, int& k1, int& run) {
+    if (t < first) {
+      tile = t;
+      t += G;
+      k0 = 0, k1 = ktiles, run = -1;
+      return true;
+    }
+    const int r = t % G;  // = cta
+    if (st == 0) {  // head of the run
+      st = 1;
+      if (hk > 0) {
+        tile = hb, k0 = 0, k1 = hk, run = r;
+        return true;
+      }
+    }
+    if (st == 1) {  // whole tiles of the run, then its tail
+      if (w < f1) {
+        tile = w++, k0 = 0, k1 = ktiles, run = r;
+        return true;
+      }
+      st = 2;
+      if (tk > 0) {
+        tile = ta, k0 = tk, k1 = ktiles, run = r;
+        return true;
+      }
+    }
+    st = 3;
+    return false;
+  }
 };
-constexpr uint32_t kDescBytes = 20;  // tm, tn, k0, k1 (v4) + run
 
 //
 // PEER: the fused GEMM -> all-gather epilogue (moa_gemm_lifted_gather). Every FINAL
@@ -344,7 +402,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ flags,
-                unsigned int* __restrict__ tile_ctr, const __grid_constant__ PeerDst peers, int oneshot) {
+                unsigned int* __restrict__ issued, const __grid_constant__ PeerDst peers, int mode) {
   using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -352,10 +410,10 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
-  const uint32_t desc0 = empty0 + STAGES * 8;  // 16-B aligned (v4 st.async)
-  volatile PieceDesc* desc = reinterpret_cast<volatile PieceDesc*>(smem_raw + (desc0 - raw));
+  const uint32_t lag0 = empty0 + STAGES * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (int)((n + kBK - 1) / kBK);
+  const bool oneshot = mode & kK1OneShot, lag = mode & kK1Lag;
 #ifdef MOA_K1_PHASES
   if (threadIdx.x == 0) MOA_PH(0, gtime());
 #endif
@@ -371,6 +429,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
+      mbar_init(lag0 + 8 * s, Tr::kConsumerWarps / 2);
     }
     fence_mbar_init();
   }
@@ -398,14 +457,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
 #ifdef MOA_K1_PHASES
           if (kt == 0) MOA_PH(2, gtime());
 #endif
-          if (kt == k0) {
-            mbar_arrive_expect_tx(fb, Tr::kStageBytes + kDescBytes);
-            const uint32_t d = desc0 + 32 * stage;
-            st_async_v4(d, (int32_t)tm, (int32_t)tn, k0, k1, fb);
-            st_async_b32(d + 16, run, fb);
-          } else {
-            mbar_arrive_expect_tx(fb, Tr::kStageBytes);
-          }
+          mbar_arrive_expect_tx(fb, Tr::kStageBytes);
           const uint32_t sa = sbase + stage * Tr::kStageBytes;
           tma_load_2d(sa, &tmA, fb, kt * kBK, row0);
 #pragma unroll
@@ -417,43 +469,20 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
           }
         }
       };
-      const int64_t tiles = tiles_m * tiles_n;
-      if (flags && !tile_ctr) {
-        // every tile is in the stream-K region (tiles < 2G): run = CTA index, no
-        // claiming (claiming cost ~4 us at N=1024 where the kernel lasts ~70 us)
-        const SkRun q = sk_run(tiles, ktiles, gridDim.x, blockIdx.x);
-        const int r = (int)blockIdx.x;
-        if (q.hk > 0) emit(q.hb, 0, q.hk, r);
-        for (int64_t w = q.f0; w < q.f1; ++w) emit(w, 0, ktiles, r);
-        if (q.tk > 0) emit(q.ta, q.tk, ktiles, r);
-      } else if (tile_ctr) {
-        const int64_t G = gridDim.x, first = flags ? sk_first_tile(tiles, G) : tiles;
-        for (;;) {
-          const int64_t t = (int64_t)atomicAdd(tile_ctr, 1u);
-          if (t < first) {
-            emit(t, 0, ktiles, -1);
-            continue;
-          }
-          const int64_t r = t - first;  // this CTA's stream-K run (at most one)
-          if (flags && r < G) {
-            const SkRun q = sk_run(tiles, ktiles, G, r);
-            if (q.hk > 0) emit(q.hb, 0, q.hk, (int)r);
-            for (int64_t w = q.f0; w < q.f1; ++w) emit(w, 0, ktiles, (int)r);
-            if (q.tk > 0) emit(q.ta, q.tk, ktiles, (int)r);
-          }
-          break;
-        }
-      } else if (oneshot) {
-        // one tile per CTA with all of k resident (ktiles <= STAGES, grid == tiles):
-        // every TMA is issued at once, no stage is reused, no end-of-work sentinel
-        emit(blockIdx.x, 0, ktiles, -1);
-      } else {
-        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) emit(t, 0, ktiles, -1);
-      }
-      if (!oneshot) {
-        mbar_wait(empty0 + 8 * stage, phase ^ 1u);  // end-of-work sentinel slot
-        mbar_arrive_expect_tx(full0 + 8 * stage, 16);
-        st_async_v4(desc0 + 32 * stage, -1, 0, 0, 0, full0 + 8 * stage);
+      const int64_t tiles = tiles_m * tiles_n, G = gridDim.x;
+      // Wave gate: the tiles of wave t/G start only once every tile of the earlier
+      // waves has had all its loads issued, so the CTAs of a wave walk k in step and
+      // share each A/B k-slab through L2 instead of drifting apart over many waves
+      // (which re-read the panels from DRAM). The last issue precedes the last
+      // consume by the ring depth, so the gate opens inside the producer's lead.
+      const bool gate = (mode & kK1WaveGate) && issued;
+      StaticSched sc(tiles, ktiles, G, blockIdx.x, flags != nullptr);
+      int64_t t;
+      int k0, k1, run;
+      while (sc.next(t, k0, k1, run)) {
+        if (gate) wave_gate(issued, (unsigned)min(t / G * G, (int64_t)sc.first));
+        emit(t, k0, k1, run);
+        if (gate && run < 0) atomicAdd(issued, 1u);  // all loads of a whole tile issued
       }
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -472,20 +501,18 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   Acc<Tr::kMA, Tr::kNBox> acc;
   int stage = 0;
   uint32_t phase = 0;
+  StaticSched sc(tiles_m * tiles_n, ktiles, gridDim.x, blockIdx.x, flags != nullptr);
   for (;;) {
-    // Peek: wait for the first stage of the next piece and read its descriptor
-    // (consume_piece waits on the same, already complete, phase again).
-    mbar_wait(full0 + 8 * stage, phase);
-    __syncwarp();
-    const int64_t tm = desc[stage].tm;
-    if (tm < 0) break;
-    const int64_t tn = desc[stage].tn;
-    const int k0 = desc[stage].k0, k1 = desc[stage].k1, run = desc[stage].run;
+    int64_t tm, tn;
+    int k0, k1, run;
+    int64_t t;
+    if (!sc.next(t, k0, k1, run)) break;
+    tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
-    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(acc, sptr, full0, empty0, stage, phase, C, m, p,
-                                                                   ldc, tm * BM, tn * BN, wm, wn, k0, k1,
-                                                                   ACC || tail, f, lane, !oneshot);
+    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes, Tr::kLag>(
+        acc, sptr, full0, empty0, lag0, lag ? warp >> 2 : -1, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1,
+        ACC || tail, f, lane, !oneshot);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
     if constexpr (PEER) {
@@ -494,7 +521,6 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
           store_acc<Tr::kMA, Tr::kNBox, true>(acc, reinterpret_cast<double*>(peers.dst[d]), m, p, ldc,
                                               tm * BM + wm * 8 * Tr::kMA, tn * BN + wn * Tr::kNBox * 16, f);
     }
-    if (oneshot) break;
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -568,6 +594,15 @@ cudaError_t k1_attrs() {
   return e;
 }
 
+// The wave gate is on by default; MOA_K1_WAVE_GATE=0 turns it off (A/B experiments).
+bool k1_wave_gate() {
+  static const bool on = [] {
+    const char* e = getenv("MOA_K1_WAVE_GATE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int BM, int BN, int WM, int WN, int ST>
 int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   using Tr = K1Traits<BM, BN, WM, WN, ST>;
@@ -594,14 +629,16 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
-  // Schedule (see the kernel): dynamic tiles, plus stream-K runs when the last
-  // wave is partial; static stride for one wave.
+  // Schedule (see the kernel): whole tiles by static stride, plus stream-K runs when
+  // the last wave is partial; a counter carries the wave gate's issue count.
   unsigned int *flags = nullptr, *ctr = nullptr;
+  const bool gate = k1_wave_gate();
   if (plan.tiles > plan.grid) {
     const bool sk = use_stream_k(plan.tiles, plan.grid);
     if (sk && !acquire_split_flags((unsigned)plan.grid + 1, stream, &flags)) return MOA_ERR_CUDA;
-    // no counter when every tile is a stream-K run (tiles < 2G: run = CTA index)
-    if (!(sk && sk_first_tile(plan.tiles, plan.grid) == 0) && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
+    const int64_t first = sk ? sk_first_tile(plan.tiles, plan.grid) : plan.tiles;
+    // the gate's issue counter, when there are at least two waves of whole tiles
+    if (gate && first >= 2 * plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)plan.grid);
@@ -614,9 +651,14 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // one tile per CTA and all of k resident in the ring: no stage is ever refilled
-  const int oneshot = (plan.tiles <= plan.grid && (n + kBK - 1) / kBK <= ST) ? 1 : 0;
+  int mode = (plan.tiles <= plan.grid && (n + kBK - 1) / kBK <= ST) ? kK1OneShot : 0;
+  if (ctr && gate) mode |= kK1WaveGate;
+  // Lag pays at shallow k (tile boundaries every <= 64 slabs: 65536x512x512 +0.7%,
+  // 16384x1024x1024 +0.25%) and costs at deep k (8192^3 -0.6%, 1024^3 with 64x64
+  // tiles -0.8%): profiles/r02_ab_lag.jsonl.
+  if (Tr::kLag && BM == 128 && (n + kBK - 1) / kBK <= 64) mode |= kK1Lag;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                     (int)plan.raster_group, flags, ctr, peers, oneshot);
+                                     (int)plan.raster_group, flags, ctr, peers, mode);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -642,10 +684,9 @@ TileConfig kK1Configs[] = {
     {MOA_KERNEL_DGEMM_TMA, 64, 32, 16, 4, K1Traits<64, 32, 2, 2, 4>::kThreads, 4, K1Traits<64, 32, 2, 2, 4>::kSmem, 0.0},
     // latency tiles (16x16 outputs per warp): eta here is the latency-regime factor;
     // the chooser considers them only for tiny problems (moa_host.cpp choose()).
-    // 16x32 first: it wins the ties (N=512: 13.2 vs 22.3 us for 16x16). Its one-shot
-    // form (16 stages = all of k <= 256 resident, one tile per CTA) goes first of all:
-    // every TMA is in flight at once and no slab pays a release (fence + arrive).
-    {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 16, K1Traits<16, 32, 1, 2, 16>::kThreads, 2, K1Traits<16, 32, 1, 2, 16>::kSmem, 1.0, 16},
+    // 16x32 first: it wins the ties (N=512: 13.2 vs 22.3 us for 16x16). (A 16-stage
+    // one-shot form, all of k <= 256 resident, was measured and dropped: 256^3 5.92 vs
+    // 5.79 us for 16x16, 512^3 24.7 vs 13.2 us: profiles/r02/small_n_k5_dfma.json.)
     {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 4, K1Traits<16, 32, 1, 2, 4>::kThreads, 8, K1Traits<16, 32, 1, 2, 4>::kSmem, 1.0},
     {MOA_KERNEL_DGEMM_TMA, 16, 16, 16, 4, K1Traits<16, 16, 1, 1, 4>::kThreads, 8, K1Traits<16, 16, 1, 1, 4>::kSmem, 1.0},
 };
@@ -667,10 +708,9 @@ void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
     RelaxedCapture relaxed_capture;
-    int o[7] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
-                k1_occupancy<64, 32, 2, 2, 4>(),   k1_occupancy<16, 32, 1, 2, 16>(), k1_occupancy<16, 32, 1, 2, 4>(),
-                k1_occupancy<16, 16, 1, 1, 4>()};
-    for (int i = 0; i < 7; ++i)
+    int o[6] = {k1_occupancy<128, 128, 4, 2, 6>(), k1_occupancy<128, 64, 4, 2, 4>(), k1_occupancy<64, 64, 2, 4, 4>(),
+                k1_occupancy<64, 32, 2, 2, 4>(),   k1_occupancy<16, 32, 1, 2, 4>(),   k1_occupancy<16, 16, 1, 1, 4>()};
+    for (int i = 0; i < 6; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
@@ -700,7 +740,6 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
   if (plan.bm == 128 && plan.bn == 64 && plan.stages == 4) return launch_k1<128, 64, 4, 2, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 64 && plan.stages == 4) return launch_k1<64, 64, 2, 4, 4>(plan, g, stream);
   if (plan.bm == 64 && plan.bn == 32 && plan.stages == 4) return launch_k1<64, 32, 2, 2, 4>(plan, g, stream);
-  if (plan.bm == 16 && plan.bn == 32 && plan.stages == 16) return launch_k1<16, 32, 1, 2, 16>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 32 && plan.stages == 4) return launch_k1<16, 32, 1, 2, 4>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 16 && plan.stages == 4) return launch_k1<16, 16, 1, 1, 4>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");

@@ -263,10 +263,6 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
   for (int i = 0; i < nc; ++i) {
     const TileConfig& c = cfgs[i];
     if (c.smem_bytes > ds.smem_optin) continue;
-    if (c.max_ktiles > 0) {  // one-shot: all of k resident, one resident CTA per tile
-      const int64_t tl = ((m + c.bm - 1) / c.bm) * ((p + c.bn - 1) / c.bn);
-      if ((n + c.bk - 1) / c.bk > c.max_ktiles || tl > (int64_t)ds.sms * c.ctas_per_sm) continue;
-    }
     double eta = c.eta;
     if (eta <= 0.0) {
       // A 32-column tile (K1 64x32) is offered only where every 64-column tile would
@@ -296,6 +292,14 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
       if (mp >= one && !thin) continue;
       const int64_t warps = tiles * ((int64_t)c.bm * c.bn / 256), smsp = 4LL * ds.sms;
       eff = mp / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * eta * (mp < one ? 1.0 : 0.85);
+      // 16x16 (one consumer + one producer warp per CTA): measured 2% ahead of 16x32
+      // while at most 4 CTAs share an SM (N = 64..384), but beyond that its consumer
+      // warps crowd 2 of the 4 SM sub-partitions (N = 512: 25.2 vs 13.2 us):
+      // profiles/r02/small_n_k5_dfma.json
+      if (c.bm * c.bn == 16 * 16) {
+        if (tiles > 4LL * ds.sms) continue;
+        eff *= 1.01;
+      }
     }
     // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
     // cut tiles cost a partial store + reload and an extra pipeline fill: -1%, and
@@ -333,6 +337,11 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
   out->smem_bytes = c.smem_bytes;
   out->sms = ds.sms;
   return MOA_OK;
+}
+
+int tile_configs_for(int kernel, const TileConfig** cfgs) {
+  if (kernel == MOA_KERNEL_DGEMM_TMA || kernel == MOA_KERNEL_DGEMM_GENERIC) return dgemm_tile_configs(kernel, cfgs);
+  return sgemm_tile_configs(kernel, cfgs);
 }
 
 int plan_impl(int64_t m, int64_t n, int64_t p, int dtype, const DeviceShape& ds, bool tma_ok, moa_plan_t* out) {
@@ -407,9 +416,7 @@ int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t
   if (plan && pl.kernel == plan->kernel) {
     // honour an explicit tile choice (the block-size experiment) if it is a compiled config
     const TileConfig* cfgs = nullptr;
-    int nc = (pl.kernel == MOA_KERNEL_DGEMM_TMA || pl.kernel == MOA_KERNEL_DGEMM_GENERIC)
-                 ? dgemm_tile_configs(pl.kernel, &cfgs)
-                 : sgemm_tile_configs(pl.kernel, &cfgs);
+    int nc = tile_configs_for(pl.kernel, &cfgs);
     bool found = false;
     for (int i = 0; i < nc && !found; ++i)
       if (cfgs[i].bm == plan->bm && cfgs[i].bn == plan->bn && cfgs[i].stages == plan->stages) {

@@ -84,9 +84,6 @@ struct TileConfig {
   int kernel;
   int bm, bn, bk, stages, threads, ctas_per_sm, smem_bytes;
   double eta;  // per-tile efficiency prior (smaller tiles: more smem/L2 traffic per flop)
-  // > 0: a one-shot config, offered only when all of k fits its ring (ceil(n/bk) <=
-  // max_ktiles) and every tile gets its own resident CTA (no stage is ever refilled)
-  int max_ktiles = 0;
 };
 // Return the number of configs for a kernel id and fill *out (static storage).
 #ifdef __CUDACC__

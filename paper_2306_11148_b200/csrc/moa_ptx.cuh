@@ -50,19 +50,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
-// Asynchronous (async-proxy) stores into this CTA's shared memory that complete
-// transaction bytes on an mbarrier, like a TMA load: the piece descriptors of K1/K3
-// travel with the stage they describe, so a consumer that has waited on the stage's
-// full barrier sees them, and no generic-proxy store races with its reads.
-__device__ __forceinline__ void st_async_v4(uint32_t dst, int32_t a, int32_t b, int32_t c, int32_t d, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
-               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void st_async_b32(uint32_t dst, int32_t a, uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst), "r"(a), "r"(bar)
-               : "memory");
-}
 // Order this thread's generic-proxy shared-memory accesses with later async-proxy
 // (TMA / tensor-core) accesses of the same bytes. Needed by every consumer that
 // reads a stage with ld.shared before releasing it to a TMA producer (WAR), and
@@ -75,23 +62,19 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 }
 // ------------------------- stream-K schedule (K1) -----------------------------
 // Balanced assignment of the (tile, k-slab) work of one launch to its G persistent
-// CTAs. The first D = (T/G - 1)*G tiles (full waves but one) are data-parallel and
-// claimed dynamically from the launch's tile counter. The last S = T - D tiles
-// (S in [G, 2G)) are cut into G equal runs of k-slabs; when a CTA's claim runs
-// past D, the value it drew minus D is its run index r. A tile cut between runs
-// r and r+1 has its low-k part ("head") at the end of run r and its high-k part
-// ("tail") at the start of run r+1.
+// CTAs. The first D = (T/G - 1)*G tiles (full waves but one) are data-parallel,
+// CTA c taking tiles c, c+G, ... (K1's static schedule, kept in k-lockstep per wave
+// by the wave gate). The last S = T - D tiles (S in [G, 2G)) are cut into G equal
+// runs of k-slabs, run r on CTA r. A tile cut between runs r and r+1 has its low-k
+// part ("head") at the end of run r and its high-k part ("tail") at the start of
+// run r+1.
 // Bitwise rule: the tail continues the fma chain from the stored low-k partial
 // (DMMA/FFMA continue the chain from their C operand), so the result equals the
 // unsplit tile. Within its run a CTA computes its head FIRST and its tail LAST.
-// Runs are claimed in counter order, so run r-1 was claimed no later than run r,
-// and with runs R >= K slabs run r reaches its tail after h_r + F_r = R - K +
-// h_{r-1} >= h_{r-1} slabs of its own: never before run r-1's head is done (in the
-// uniform-speed model; otherwise it waits on the flag, and there is no cycle:
-// run 0 has no tail).
-// Dynamic claiming of the data-parallel tiles keeps all CTAs of a wave in
-// k-lockstep (they share the A/B k-slabs in L2) and absorbs SM speed variance; the
-// runs remove the last partial wave.
+// With runs R >= K slabs, run r reaches its tail after h_r + F_r = R - K + h_{r-1}
+// >= h_{r-1} slabs of its own: never before run r-1's head is done (in the
+// uniform-speed model; otherwise it waits on the flag, and there is no cycle: run 0
+// has no tail).
 __host__ __device__ __forceinline__ int64_t sk_first_tile(int64_t tiles, int64_t G) {
   return tiles >= 2 * G ? (tiles / G - 1) * G : 0;
 }
@@ -133,6 +116,16 @@ __device__ __forceinline__ void split_wait(const unsigned int* flag, unsigned in
   __syncwarp();
   __threadfence();
 }
+// K1's wave gate: spin (one producer thread) until `need` whole tiles have had all
+// their loads issued.
+__device__ __forceinline__ void wave_gate(const unsigned int* issued, unsigned int need) {
+  unsigned int v;
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(issued) : "memory");
+    if (v >= need) break;
+    __nanosleep(128);
+  }
+}
 __device__ __forceinline__ void split_release(unsigned int* flag, unsigned int total, int lane) {
   __syncwarp();
   if (lane == 0 && atomicAdd(flag, 1u) == total - 1) atomicExch(flag, 0u);
@@ -161,9 +154,10 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* 
                int box_cols, int box_rows, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B,
                int64_t ld = -1 /* row stride in elements; -1 = cols */);
 
-// Host: a zeroed device counter for one dynamically scheduled launch on `stream`
-// (a slot of a per-device pool allocated once; zeroed with cudaMemsetAsync on the
-// stream, so it is ordered before the kernel). Returns false (error set) on failure.
+// Host: a zeroed device counter for one launch on `stream` (a slot of a per-device
+// pool allocated once; zeroed with cudaMemsetAsync on the stream, so it is ordered
+// before the kernel): K1's wave gate counts the whole tiles whose loads are all
+// issued in it. Returns false (error set) on failure.
 bool acquire_tile_counter(cudaStream_t stream, unsigned int** out);
 // Host: `count` zeroed split-tile flags for one stream-K launch (a window of a
 // per-device ring, zeroed once at creation; every launch leaves its flags at 0 —

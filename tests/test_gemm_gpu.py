@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 # every compiled K1 tile config (bm, bn, stages), incl. the latency tiles
-K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 16), (16, 32, 4), (16, 16, 4)]
+K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
 
 
 def _moa():
@@ -185,25 +185,46 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
         assert _bits_equal(out.cpu().numpy(), ref), (bm, bn, st)
 
 
-@pytest.mark.parametrize("shape", [(256, 256, 256), (250, 256, 250), (1, 16, 2), (17, 254, 34), (160, 96, 480),
-                                   (300, 200, 260)])
-def test_oneshot_latency_tiles_bitwise(cuda_device, shape):
-    """Tiny problems (configs[0], 256^3): the chooser's one-shot 16x32 latency tile
-    (all of k resident in a 16-stage ring, one tile per CTA, no stage release) gives
-    the fused ip.c bits, ragged edges included; the literal ip.c within 1e-12 sqrt(n)."""
+@pytest.mark.parametrize("shape", [(256, 256, 256), (250, 256, 250), (1, 16, 2), (17, 254, 34), (160, 48, 480),
+                                   (300, 200, 260), (512, 512, 512), (96, 600, 130)])
+def test_latency_tiles_bitwise(cuda_device, shape):
+    """Tiny problems (configs[0], 256^3): the chooser's latency tiles (16x16 while at
+    most 4 CTAs share an SM, else 16x32; one tile per CTA; with all of k in the ring —
+    n <= 64 here — no stage is ever released) give the fused ip.c bits, ragged edges
+    included, and the literal ip.c within 1e-12 sqrt(n); every latency config does;
+    a two-panel accumulate chain started from +0 is the same chain; the fused-gather
+    epilogue writes the same bits to an extra destination."""
     import torch
     moa = _moa()
     m, n, p = shape
     A, B = _host(m, n, p, 31)
+    ref = O.ip(A, B, fused=True)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
     pl = moa.plan(m, n, p)
-    assert (pl.bm, pl.bn, pl.stages) == (16, 32, 16), pl
+    t16 = -(-m // 16) * -(-p // 16)
+    assert (pl.bm, pl.bn) == ((16, 16) if t16 <= 4 * pl.sms else (16, 32)), pl
     assert pl.grid == pl.tiles
-    out = moa.gemm(torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device))
-    torch.cuda.synchronize()
-    got = out.cpu().numpy()
-    assert _bits_equal(got, O.ip(A, B, fused=True))
+    got = moa.gemm(tA, tB).cpu().numpy()
+    assert _bits_equal(got, ref)
     lit = O.ip(A, B, fused=False)
     assert np.linalg.norm(got - lit) <= 1e-12 * np.sqrt(n) * np.linalg.norm(lit)
+    for (bm, bn, st) in [(16, 32, 4), (16, 16, 4)]:
+        q = moa.Plan(**{**pl.__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
+        out = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+        moa.gemm_with_plan(tA, tB, out, q)
+        torch.cuda.synchronize()
+        assert _bits_equal(out.cpu().numpy(), ref), (bm, bn)
+    k0 = (n // 2) // 2 * 2
+    out = torch.zeros((m, p), dtype=torch.float64, device=cuda_device)
+    moa.gemm_acc(tA[:, :k0], tB[:k0], out, True)
+    moa.gemm_acc(tA[:, k0:], tB[k0:], out, True)
+    torch.cuda.synchronize()
+    assert _bits_equal(out.cpu().numpy(), ref)
+    D = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+    Cd = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
+    moa.gemm_scatter(tA, tB, Cd, [D])
+    torch.cuda.synchronize()
+    assert _bits_equal(Cd.cpu().numpy(), ref) and _bits_equal(D.cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("shape", [(2000, 200, 2000), (1500, 100, 3000), (2100, 56, 1030)])
@@ -243,9 +264,9 @@ def test_plan_is_static_and_sane(cuda_device):
     for (m, n, p) in [(256, 256, 256), (1024, 1024, 1024), (8192, 8192, 8192), (16384, 16384, 16384),
                       (65536, 512, 512)]:
         pl = moa.plan(m, n, p)
-        assert pl.kernel == "dgemm_tma" and pl.bk == 16
+        assert pl.kernel == "dgemm_tma" and pl.bk == 16, pl
         assert pl.tiles == -(-m // pl.bm) * -(-p // pl.bn)
-        assert 1 <= pl.grid <= pl.sms * pl.ctas_per_sm and pl.ctas_per_sm >= 1
+        assert 1 <= pl.grid <= max(pl.tiles, pl.sms * pl.ctas_per_sm) and pl.ctas_per_sm >= 1
         assert moa.plan(m, n, p) == pl
     assert moa.plan(16384, 16384, 16384).bm == 128
     assert moa.plan(5, 7, 9).kernel == "dgemm_generic"  # odd n / p: not describable by TMA

@@ -19,13 +19,16 @@ import torch
 lib = ctypes.CDLL(%r)
 lib.moa_gemm.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_void_p]
 from inputs import inputs as I
+import os
+DT = int(os.environ.get("AB_DTYPE", "0"))  # 0 fp64, 1 exact fp32, 2 3xTF32 (moa.h moa_dtype)
+tt = torch.float64 if DT == 0 else torch.float32
 res, sums = {}, {}
 for (m, n, p) in %r:
-    A = torch.empty((m, n), dtype=torch.float64, device="cuda"); B = torch.empty((n, p), dtype=torch.float64, device="cuda")
-    C = torch.empty((m, p), dtype=torch.float64, device="cuda")
+    A = torch.empty((m, n), dtype=tt, device="cuda"); B = torch.empty((n, p), dtype=tt, device="cuda")
+    C = torch.empty((m, p), dtype=tt, device="cuda")
     I.device_fill(A, 1, I.ID_A); I.device_fill(B, 1, I.ID_B)
     s = torch.cuda.current_stream().cuda_stream
-    f = lambda: lib.moa_gemm(m, n, p, A.data_ptr(), B.data_ptr(), C.data_ptr(), 0, s)
+    f = lambda: lib.moa_gemm(m, n, p, A.data_ptr(), B.data_ptr(), C.data_ptr(), DT, s)
     for _ in range(3): f()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -38,7 +41,7 @@ for (m, n, p) in %r:
     ms = a.elapsed_time(b) / reps
     key = "%%dx%%dx%%d" %% (m, n, p)
     res[key] = round(2 * m * n * p / (ms / 1e3) / 1e12, 3)
-    sums[key] = hashlib.sha1(C.view(torch.int64).cpu().numpy().tobytes()).hexdigest()[:12]
+    sums[key] = hashlib.sha1(C.view(torch.int64 if DT == 0 else torch.int32).cpu().numpy().tobytes()).hexdigest()[:12]
 print(json.dumps({"tflops": res, "bits": sums}))
 '''
 

@@ -20,7 +20,8 @@ import paper_2306_11148_b200 as moa  # noqa: E402
 from inputs import inputs as I  # noqa: E402
 
 PEAK = 37.0
-CFGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 16), (16, 32, 4), (16, 16, 4)]
+CFGS = [("dgemm_tma", 128, 128, 6), ("dgemm_tma", 128, 64, 4), ("dgemm_tma", 64, 64, 4), ("dgemm_tma", 64, 32, 4),
+        ("dgemm_tma", 16, 32, 4), ("dgemm_tma", 16, 16, 4)]
 
 
 def time_fn(fn, reps):
@@ -72,18 +73,18 @@ def main():
         pl = moa.plan(N, N, N)
         fl = 2.0 * N ** 3
         reps = max(5, min(2000, int(0.3 / (fl / 30e12))))
-        row = {"N": N, "chosen": [pl.bm, pl.bn, pl.stages], "cfgs": []}
-        for bm, bn, st in CFGS:
-            q = moa.Plan(**{**pl.__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
+        row = {"N": N, "chosen": [pl.kernel, pl.bm, pl.bn, pl.stages], "cfgs": []}
+        for kern, bm, bn, st in CFGS:
+            q = moa.Plan(**{**pl.__dict__, "kernel": kern, "bm": bm, "bn": bn, "stages": st, "grid": 0})
             fn = lambda: moa.gemm_with_plan(A, B, C, q)  # noqa: E731
             try:
                 e = time_fn(fn, reps)
                 g = time_graph(fn, min(reps, 200)) if N <= 4096 else e
             except moa.MoAError as ex:
-                row["cfgs"].append({"cfg": [bm, bn, st], "error": str(ex)})
+                row["cfgs"].append({"cfg": [kern, bm, bn, st], "error": str(ex)})
                 continue
             ok = torch.equal(C, ref)
-            row["cfgs"].append({"cfg": [bm, bn, st], "eager_us": round(e * 1e3, 2), "graph_us": round(g * 1e3, 2),
+            row["cfgs"].append({"cfg": [kern, bm, bn, st], "eager_us": round(e * 1e3, 2), "graph_us": round(g * 1e3, 2),
                                 "frac_graph": round(fl / (g / 1e3) / 1e12 / PEAK, 4), "bitwise": ok})
         out.append(row)
         print(json.dumps(row), file=sys.stderr)
