@@ -249,15 +249,7 @@ struct K1Traits {
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // Lagged consumer groups (8 consumer warps): warps 4..7 consume each stage only
-  // after warps 0..3 have (one lag barrier per stage), so the two warps of every SM
-  // sub-partition are a slab apart and never cross a tile boundary together.
-#ifdef MOA_K1_NO_LAG  // A/B variant builds only
-  static constexpr bool kLag = false;
-#else
-  static constexpr bool kLag = kConsumerWarps == 8;
-#endif
-  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 3 * STAGES * 8;  // + full/empty/lag barriers
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8;  // + full/empty barriers
   static_assert(BM == 8 * kMA * WARPS_M && (kMA == 1 || kMA == 2 || kMA == 4), "warp tile is 8, 16 or 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -267,17 +259,12 @@ struct K1Traits {
 // low-k partial of a split tile), else from +0: the loads are predicated off by
 // passing m = 0, so there is ONE copy of the slab loop in the kernel (a branch
 // between load_acc and acc_zero once cost 5.4% in register copies).
-// Lag (8 consumer warps, kLag): group 0 (warps 0..3) arrives on lag[stage] after its
-// slab; group 1 (warps 4..7) waits on it before its own. One warp of each group sits
-// on every SM sub-partition (SMSP = warp % 4), so while one group is at a tile
-// boundary (drain the DMMA chains, store C, read the next piece) the other still
-// has a slab of DMMAs for that SMSP's pipe.
-template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES, bool LAG>
+template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
-                                              uint32_t lag0, int group, int& stage, uint32_t& phase,
+                                              int& stage, uint32_t& phase,
                                               double* __restrict__ C, int64_t m, int64_t p, int64_t ldc,
                                               int64_t row0, int64_t col0, int wm, int wn, int k0, int k1, bool load,
-                                              const FragOffsets& f, int lane, bool release) {
+                                              const FragOffsets& f, int lane) {
   load_acc<MA, NBOX, true>(acc, C, load ? m : 0, p, ldc, row0 + wm * 8 * MA, col0 + wn * NBOX * 16, f);
 #ifdef MOA_K1_PHASES
   unsigned long long waited = 0, tw0 = 0;
@@ -288,7 +275,6 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
     if (ph) tw0 = gtime();
 #endif
     mbar_wait(full0 + 8 * stage, phase);  // (ptxas reconverges the spin with BSSY/BSYNC before the DMMAs)
-    if (LAG && group > 0) mbar_wait(lag0 + 8 * stage, phase);  // (group -1: this launch runs without lag)
 #ifdef MOA_K1_PHASES
     if (ph) {
       const unsigned long long tw1 = gtime();
@@ -298,19 +284,14 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
 #endif
     const uint8_t* sa = sptr + stage * STAGE_BYTES;
     mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
-    if (LAG && group == 0 && lane == 0) mbar_arrive(lag0 + 8 * stage);  // (no data: ordering of progress only)
     // WAR across proxies: these generic-proxy LDS reads must be ordered before the
     // producer's next TMA (async-proxy) write of this stage. The arrive's .release
     // alone does not do it (ptxas even hoists the arrive above the slab's last
     // DMMAs): without this fence whole warp tiles were computed from overwritten
     // operands, rarely under dynamic scheduling, often under stream-K.
-    // A one-shot launch (one tile per CTA, all of k resident: no stage is ever
-    // refilled) skips the release entirely.
-    if (release) {
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * stage);
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1u;
@@ -339,9 +320,7 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
 // wave gate (producer) keeps the CTAs of a wave in k-lockstep, which round 1's
 // dynamic tile claiming only approximated.
 // launch mode bits (host -> K1)
-constexpr int kK1OneShot = 1;   // one tile per CTA, all of k resident: no stage release
 constexpr int kK1WaveGate = 2;  // wave gate (see the producer)
-constexpr int kK1Lag = 8;       // lagged consumer groups (8-warp tiles, shallow k)
 
 // One CTA's static schedule: whole tiles cta, cta + G, ... below
 // `first` (the stream-K region's start, or all tiles), then its stream-K run r = cta:
@@ -410,10 +389,8 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   const uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
-  const uint32_t lag0 = empty0 + STAGES * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (int)((n + kBK - 1) / kBK);
-  const bool oneshot = mode & kK1OneShot, lag = mode & kK1Lag;
 #ifdef MOA_K1_PHASES
   if (threadIdx.x == 0) MOA_PH(0, gtime());
 #endif
@@ -429,7 +406,6 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
-      mbar_init(lag0 + 8 * s, Tr::kConsumerWarps / 2);
     }
     fence_mbar_init();
   }
@@ -507,12 +483,13 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     int k0, k1, run;
     int64_t t;
     if (!sc.next(t, k0, k1, run)) break;
+    // (the 64-bit map: a 32-bit one was measured 0.6% slower at 8192^3 through the
+    // consumers' code generation, profiles/r02/ab_bisect*.jsonl)
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
-    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes, Tr::kLag>(
-        acc, sptr, full0, empty0, lag0, lag ? warp >> 2 : -1, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1,
-        ACC || tail, f, lane, !oneshot);
+    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(
+        acc, sptr, full0, empty0, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1, ACC || tail, f, lane);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
     if constexpr (PEER) {
@@ -651,12 +628,8 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // one tile per CTA and all of k resident in the ring: no stage is ever refilled
-  int mode = (plan.tiles <= plan.grid && (n + kBK - 1) / kBK <= ST) ? kK1OneShot : 0;
+  int mode = 0;
   if (ctr && gate) mode |= kK1WaveGate;
-  // Lag pays at shallow k (tile boundaries every <= 64 slabs: 65536x512x512 +0.7%,
-  // 16384x1024x1024 +0.25%) and costs at deep k (8192^3 -0.6%, 1024^3 with 64x64
-  // tiles -0.8%): profiles/r02_ab_lag.jsonl.
-  if (Tr::kLag && BM == 128 && (n + kBK - 1) / kBK <= 64) mode |= kK1Lag;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
                                      (int)plan.raster_group, flags, ctr, peers, mode);
   if (e == cudaSuccess) e = cudaGetLastError();

@@ -163,15 +163,9 @@ struct K3Traits {
   static constexpr int kABytes = BM * kRowB;
   static constexpr int kBBytes = kBKf * BN * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // lagged consumer groups, as K1: warps 4..7 consume each stage only after warps
-  // 0..3 have, so the two warps of an SM sub-partition reach the slab boundary
-  // (barrier wait, fence, release) a slab apart and the FMA pipe stays fed
-#ifdef MOA_K3_NO_LAG  // A/B variant builds only
-  static constexpr bool kLag = false;
-#else
-  static constexpr bool kLag = true;
-#endif
-  static constexpr int kSmem = 1024 + STAGES * kStageBytes + 3 * STAGES * 8;
+  // (Lagged consumer groups as in K1 were measured here too: -0.15% at 4096^3 to
+  // 16384^3, profiles/r02/ab_k3_lag.jsonl; not taken.)
+  static constexpr int kSmem = 1024 + STAGES * kStageBytes + 2 * STAGES * 8;
 };
 
 // ACC is compile-time so the plain path keeps its register allocation. PEER: the
@@ -189,7 +183,6 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
   const uint8_t* sptr = smem_raw + (sbase - raw);
   const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
-  const uint32_t lag0 = empty0 + STAGES * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tiles = tiles_m * tiles_n;
   const int ktiles = (int)((n + kBKf - 1) / kBKf);
@@ -199,7 +192,6 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
-      mbar_init(lag0 + 8 * s, Tr::kConsumerWarps / 2);
     }
     fence_mbar_init();
   }
@@ -246,10 +238,8 @@ __global__ void __launch_bounds__(K3Traits<STAGES>::kThreads, 1)
       sacc_zero(acc);
     for (int kt = 0; kt < ktiles; ++kt) {
       mbar_wait(full0 + 8 * stage, phase);
-      if (Tr::kLag && warp >= 4) mbar_wait(lag0 + 8 * stage, phase);
       const uint8_t* sa = sptr + stage * Tr::kStageBytes;
       ffma_slab(acc, sa, sa + Tr::kABytes, ty, tx);
-      if (Tr::kLag && warp < 4 && lane == 0) mbar_arrive(lag0 + 8 * stage);
       fence_proxy_async_smem();  // LDS reads before the producer's next TMA write (WAR)
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * stage);

@@ -67,7 +67,8 @@ def _operands(m, n, p, seed, dev):
 
 # (shape, what it exercises, the chooser's (bm, bn) for it or None)
 _SHAPES = [
-    ((200, 144, 176), "latency tiles 16x32", (16, 32)),
+    ((200, 144, 176), "latency tiles 16x16", (16, 16)),
+    ((512, 96, 512), "latency tiles 16x32", (16, 32)),
     ((1920, 1024, 1920), "128x128 stream-K only (split tiles)", (128, 128)),
     ((2560, 1024, 2560), "128x128 dynamic tiles + stream-K runs", (128, 128)),
     ((2000, 48, 2000), "64x32 shallow k, stream-K over 3 CTAs per SM", (64, 32)),

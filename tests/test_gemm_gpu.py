@@ -189,8 +189,7 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
                                    (300, 200, 260), (512, 512, 512), (96, 600, 130)])
 def test_latency_tiles_bitwise(cuda_device, shape):
     """Tiny problems (configs[0], 256^3): the chooser's latency tiles (16x16 while at
-    most 4 CTAs share an SM, else 16x32; one tile per CTA; with all of k in the ring —
-    n <= 64 here — no stage is ever released) give the fused ip.c bits, ragged edges
+    most 4 CTAs share an SM, else 16x32; one tile per CTA) give the fused ip.c bits, ragged edges
     included, and the literal ip.c within 1e-12 sqrt(n); every latency config does;
     a two-panel accumulate chain started from +0 is the same chain; the fused-gather
     epilogue writes the same bits to an extra destination."""

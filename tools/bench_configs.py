@@ -53,6 +53,9 @@ def timed(fn, window_s, sampler, est_s):
             out["j_per_gemm_above_idle"] = round(((e1 - e0) / 1e3 - IDLE_W[0] * ms * reps / 1e3) / reps, 6)
     summ = sampler.summary()
     out["temp_c_max"] = summ.get("temp_c_max")
+    out["sm_mhz"] = summ.get("sm_mhz")
+    out["power_w_median"] = summ.get("power_w_median")
+    out["throttle"] = summ.get("reasons")
     return out
 
 
@@ -72,6 +75,9 @@ def rec(m, n, p, r, peak):
     fl = 2.0 * m * n * p
     r["gflops"] = round(fl / (r["ms"] / 1e3) / 1e9, 1)
     r["frac_of_peak"] = round(fl / (r["ms"] / 1e3) / 1e12 / peak, 4)
+    if peak == FP64_DMMA_PEAK_TFLOPS and r.get("sm_mhz"):
+        # DMMA nominal at the SM clock the window actually ran at: 148 SMs x 128 flop/clk
+        r["frac_of_nominal_at_clock"] = round(fl / (r["ms"] / 1e3) / (148 * 128 * r["sm_mhz"] * 1e6), 4)
     r["hbm_gbs_algorithmic"] = None
     return r
 

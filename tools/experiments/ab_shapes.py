@@ -51,14 +51,18 @@ def main():
     libs = sys.argv[2:]
     rounds = int(os.environ.get("AB_ROUNDS", "2"))
     for rnd in range(rounds):
-        for lib in libs:
+        for spec in libs:
+            # LIB[@VAR=VAL,...]: extra environment for this build's process (e.g. MOA_K1_WAVE_GATE=0)
+            lib, _, envs = spec.partition("@")
+            env = dict(os.environ, **dict(kv.split("=", 1) for kv in envs.split(",") if kv))
             out = subprocess.run([sys.executable, "-c", CODE % (ROOT, os.path.abspath(lib), shapes)],
-                                 capture_output=True, text=True)
+                                 capture_output=True, text=True, env=env)
             try:
                 d = json.loads(out.stdout.strip().splitlines()[-1])
             except Exception:
                 d = {"error": out.stderr[-500:]}
-            print(json.dumps({"lib": os.path.basename(lib), "round": rnd, **d}), flush=True)
+            print(json.dumps({"lib": os.path.basename(lib) + ("@" + envs if envs else ""), "round": rnd, **d}),
+                  flush=True)
 
 
 if __name__ == "__main__":

@@ -19,7 +19,7 @@ import paper_2306_11148_b200 as moa  # noqa: E402
 from inputs import inputs as I  # noqa: E402
 
 SHAPES = {"c0": (256, 256, 256, torch.float64), "c3": (65536, 512, 512, torch.float64),
-          "c16k": (16384, 16384, 16384, torch.float64), "f32": (16384, 16384, 16384, torch.float32),
+          "c16k": (16384, 16384, 16384, torch.float64), "c8k": (8192, 8192, 8192, torch.float64), "f32": (16384, 16384, 16384, torch.float32),
           "tf32": (16384, 16384, 16384, torch.float32), "had": (16384, 16384, 0, torch.float64),
           "kron": (128, 128, 128, torch.float64),
           # BASELINE configs[4]: rank 0's rows of the row-lifted 32768^3 at G = 1, 2, 4, 8
