@@ -500,7 +500,7 @@ def main(argv=None):
     # energy (NVML; J per GEMM step summed over every participating GPU)
     energy = None
     ej = sum_over_ranks((e1 - e0) / 1e3 if (e0 is not None and e1 is not None) else -1e30)
-    if ej >= 0:
+    if ej > 0:  # (a window shorter than NVML's energy-counter update reads 0 J: no energy figure)
         idle_j = (idle_w_sum or 0.0) * (elapsed_ms / 1e3)
         energy = {"j_per_gemm": round(ej / args.steps, 3), "idle_w_all_gpus": idle_w_sum,
                   "j_per_gemm_above_idle": round((ej - idle_j) / args.steps, 3) if idle_w_sum is not None else None,
@@ -575,8 +575,8 @@ def main(argv=None):
             for _ in range(3):
                 moa.gemm(As, Bs, out=Cs)
             torch.cuda.synchronize()
-            est = 2.0 * Ns ** 3 / (FP64_DMMA_PEAK_TFLOPS * 0.9e12)
-            reps = max(3, math.ceil(1.05 / est))  # each window >= 1 s (NVML energy granularity)
+            est = 2.0 * Ns ** 3 / (FP64_DMMA_PEAK_TFLOPS * 1e12)  # a lower bound on the GEMM's time
+            reps = max(3, math.ceil(1.1 / est))  # so each window is >= 1.1 s (NVML energy granularity)
             wins = []
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             for _ in range(args.sweep_windows):
