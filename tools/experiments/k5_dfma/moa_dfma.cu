@@ -1,8 +1,8 @@
 // ARCHIVED EXPERIMENT (round 2) — not built, not part of libmoa.so. Compiled into the
 // library for one measurement (profiles/r02/small_n_k5_dfma.json, tools/small_n.py):
 // the DFMA latency tiles were SLOWER than K1's DMMA latency tiles at every N from 64
-// to 1024 (256^3: 7.06 vs 5.79 us graph-timed), i.e. a dependent DFMA costs more per
-// k (~43 cycles) than a dependent DMMA.8x8x4 per 4 k (~143 cycles). Kept as the
+// to 1024 (256^3: 7.06 vs 5.79 us graph-timed). Its loop is bound by its shared-memory
+// loads, not by the DFMA latency (8 cycles, tools/probe/chain_latency.cu). Kept as the
 // evidence behind DESIGN.md's small-N reading; to rebuild it, restore the
 // MOA_KERNEL_DGEMM_DFMA plumbing of commit "K5 experiment" (moa_host.cpp choose_dfma).
 // moa_dfma.cu — K5: fp64 MoA-ONF GEMM latency tiles on the FP64 SIMT pipe (DFMA).
