@@ -9,17 +9,12 @@
 //
 //   C[(i*p)+j] := sum_k A[(i*n)+k] * B[(k*p)+j]      (Eq. 3)
 //
-// Why a second fp64 kernel. Parity is bitwise against Fig. 3 ip.c with its update
-// fused (reading R3): every element is ONE fma chain, k = 0..n-1 ascending, so the
-// chain cannot be split. On the tensor core that chain is n/4 dependent DMMA.8x8x4,
-// and the measured DMMA dependent-issue time is ~140 cycles (K1 phase breakdown at
-// 256^3: 292 ns per 16-k slab with 4 independent chains per warp,
-// profiles/r02_phases.jsonl). For tiny problems the chain, not the tensor pipe, is
-// the bound: 256^3 spends 5.5 us in 64 dependent DMMAs while its flops need 0.9 us.
-// A DFMA chain runs the same arithmetic (one rounding per (i,j,k), k ascending —
-// bitwise the DMMA result and the fused oracle) at the FP64 pipe's much shorter
-// dependent latency, so K5 serves the latency regime and K1 everything else; the
-// static chooser picks between them (moa_host.cpp choose_dfma).
+// Why it was tried. Parity is bitwise against Fig. 3 ip.c with its update fused
+// (reading R3): every element is ONE fma chain, k = 0..n-1 ascending, so the chain
+// cannot be split. The hypothesis was that the n/4 dependent DMMA.8x8x4 of that chain
+// bound tiny problems; the direct probe later showed a dependent DMMA takes only 26
+// cycles (tools/probe/chain_latency.cu), so the hypothesis was wrong, and this kernel
+// (bitwise the same chain on DFMA) lost at every size.
 //
 // Structure: one tile per CTA (grid = tiles, tile t = blockIdx.x in K1's grouped
 // raster order). One producer warp streams A row segments and B row boxes with TMA
