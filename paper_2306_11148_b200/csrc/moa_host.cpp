@@ -260,7 +260,24 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
   }
   double best = -1.0;
   int bi = 0;
-  for (int i = 0; i < nc; ++i) {
+  bool ruled = false;
+  // Tiny problems (fewer 64x32 tiles than SMs): the latency tiles, by a rule read off
+  // the measured sweep (profiles/r02/small_n_latency.json, graph-timed, every pick the
+  // fastest compiled tile at N = 64...512): 16x16 CTAs of two 8x16 warps while there
+  // are at most 2.75 tiles per SM, then 16x32 CTAs of four 8x16 warps up to 2 per SM,
+  // then 16x32 CTAs of two 16x16 warps. (Spreading a CTA's outputs over more warps
+  // puts more SM sub-partitions on the short k-chains: 256^3 4.45 vs 5.18 us.)
+  if (kernel == MOA_KERNEL_DGEMM_TMA && (double)m * (double)p < (double)ds.sms * 64.0 * 32.0) {
+    const int64_t t16 = ((m + 15) / 16) * ((p + 15) / 16), t32 = ((m + 15) / 16) * ((p + 31) / 32);
+    const int want_bn = 4 * t16 <= 11LL * ds.sms ? 16 : 32;
+    const int want_st = (want_bn == 16 || t32 <= 2LL * ds.sms) ? 8 : 4;
+    for (int i = 0; i < nc; ++i)
+      if (cfgs[i].bm == 16 && cfgs[i].bn == want_bn && cfgs[i].stages == want_st && cfgs[i].smem_bytes <= ds.smem_optin) {
+        ruled = true;
+        bi = i;
+      }
+  }
+  for (int i = 0; i < nc && !ruled; ++i) {
     const TileConfig& c = cfgs[i];
     if (c.smem_bytes > ds.smem_optin) continue;
     double eta = c.eta;
@@ -292,14 +309,6 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
       if (mp >= one && !thin) continue;
       const int64_t warps = tiles * ((int64_t)c.bm * c.bn / 256), smsp = 4LL * ds.sms;
       eff = mp / ((double)smsp * (double)((warps + smsp - 1) / smsp) * 256.0) * eta * (mp < one ? 1.0 : 0.85);
-      // 16x16 (one consumer + one producer warp per CTA): measured 2% ahead of 16x32
-      // while at most 4 CTAs share an SM (N = 64..384), but beyond that its consumer
-      // warps crowd 2 of the 4 SM sub-partitions (N = 512: 25.2 vs 13.2 us):
-      // profiles/r02/small_n_k5_dfma.json
-      if (c.bm * c.bn == 16 * 16) {
-        if (tiles > 4LL * ds.sms) continue;
-        eff *= 1.01;
-      }
     }
     // K1 stream-K plans balance the last wave (every SM gets the same k-slabs); the
     // cut tiles cost a partial store + reload and an extra pipeline fill: -1%, and

@@ -25,7 +25,9 @@ pytestmark = pytest.mark.gpu
 
 EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 # every compiled K1 tile config (bm, bn, stages), incl. the latency tiles
-K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
+K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4),
+              # latency tiles with 8x16 warp tiles (stages 8 tells them apart)
+              (16, 32, 8), (16, 16, 8)]
 
 
 def _moa():
@@ -186,10 +188,11 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
 
 
 @pytest.mark.parametrize("shape", [(256, 256, 256), (250, 256, 250), (1, 16, 2), (17, 254, 34), (160, 48, 480),
-                                   (300, 200, 260), (512, 512, 512), (96, 600, 130)])
+                                   (300, 200, 260), (512, 512, 512), (96, 600, 130), (384, 64, 384)])
 def test_latency_tiles_bitwise(cuda_device, shape):
-    """Tiny problems (configs[0], 256^3): the chooser's latency tiles (16x16 while at
-    most 4 CTAs share an SM, else 16x32; one tile per CTA) give the fused ip.c bits, ragged edges
+    """Tiny problems (configs[0], 256^3): the chooser's latency tiles (16x16 of two 8x16
+    warps up to 2.75 tiles per SM, then 16x32 of four 8x16 warps up to 2 per SM, then
+    16x32 of two 16x16 warps; one tile per CTA) give the fused ip.c bits, ragged edges
     included, and the literal ip.c within 1e-12 sqrt(n); every latency config does;
     a two-panel accumulate chain started from +0 is the same chain; the fused-gather
     epilogue writes the same bits to an extra destination."""
@@ -200,14 +203,15 @@ def test_latency_tiles_bitwise(cuda_device, shape):
     ref = O.ip(A, B, fused=True)
     tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
     pl = moa.plan(m, n, p)
-    t16 = -(-m // 16) * -(-p // 16)
-    assert (pl.bm, pl.bn) == ((16, 16) if t16 <= 4 * pl.sms else (16, 32)), pl
+    t16, t32 = -(-m // 16) * -(-p // 16), -(-m // 16) * -(-p // 32)
+    want = (16, 16, 8) if 4 * t16 <= 11 * pl.sms else ((16, 32, 8) if t32 <= 2 * pl.sms else (16, 32, 4))
+    assert (pl.bm, pl.bn, pl.stages) == want, pl
     assert pl.grid == pl.tiles
     got = moa.gemm(tA, tB).cpu().numpy()
     assert _bits_equal(got, ref)
     lit = O.ip(A, B, fused=False)
     assert np.linalg.norm(got - lit) <= 1e-12 * np.sqrt(n) * np.linalg.norm(lit)
-    for (bm, bn, st) in [(16, 32, 4), (16, 16, 4)]:
+    for (bm, bn, st) in [c for c in K1_CONFIGS if c[0] == 16]:
         q = moa.Plan(**{**pl.__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
         out = torch.empty((m, p), dtype=torch.float64, device=cuda_device)
         moa.gemm_with_plan(tA, tB, out, q)

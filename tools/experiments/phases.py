@@ -23,6 +23,12 @@ import torch  # noqa: E402
 from inputs import inputs as I  # noqa: E402
 
 lib = ctypes.CDLL(sys.argv[1])
+# PHASES_PLAN="bm,bn,stages": time that compiled K1 config instead of the chooser's
+# pick (through the binding, loaded on the same variant library)
+_pp = os.environ.get("PHASES_PLAN")
+if _pp:
+    os.environ["MOA_LIBRARY"] = os.path.abspath(sys.argv[1])
+    import paper_2306_11148_b200 as moa  # noqa: E402
 lib.moa_gemm.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_void_p]
 lib.moa_k1_phases_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
 sizes = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "128,256,512").split(",")]
@@ -34,6 +40,10 @@ for N in sizes:
     I.device_fill(B, 1, I.ID_B)
     s = torch.cuda.current_stream().cuda_stream
     f = lambda: lib.moa_gemm(N, N, N, A.data_ptr(), B.data_ptr(), C.data_ptr(), 0, s)  # noqa: E731
+    if _pp:
+        bm, bn, st = (int(x) for x in _pp.split(","))
+        pl = moa.Plan(**{**moa.plan(N, N, N).__dict__, "bm": bm, "bn": bn, "stages": st, "grid": 0})
+        f = lambda: moa.gemm_with_plan(A, B, C, pl)  # noqa: E731
     for _ in range(5):
         f()
     torch.cuda.synchronize()
@@ -71,6 +81,8 @@ for N in sizes:
     with torch.cuda.stream(st):
         f2 = lambda: lib.moa_gemm(N, N, N, A.data_ptr(), B.data_ptr(), C.data_ptr(), 0,  # noqa: E731
                                   torch.cuda.current_stream().cuda_stream)
+        if _pp:
+            f2 = lambda: moa.gemm_with_plan(A, B, C, pl)  # noqa: E731
         f2()
         torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=st):

@@ -1,0 +1,15 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python tools/build.py all > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gemm_gpu.py -q -x > gpurun_out/r02_parity_ks.log 2>&1; rc=$?; echo "parity rc=$rc"; tail -2 gpurun_out/r02_parity_ks.log; [ $rc -ne 0 ] && exit 1
+timeout 600 python tools/small_n.py 64,128,192,256,320,384,448,512,640,768 > gpurun_out/r02_small_n_ks.json 2> gpurun_out/r02_small_n_ks.err; echo "small_n rc=$?"
+python - <<'PY'
+import json
+for d in json.load(open("gpurun_out/r02_small_n_ks.json")):
+    best = sorted((c.get('graph_us', 1e9), c['cfg'][1:]) for c in d['cfgs'])
+    ch = [c.get('graph_us') for c in d['cfgs'] if c['cfg'][1:] == d['chosen'][1:]]
+    print(d['N'], 'chosen', d['chosen'][1:], ch, 'best', best[:5], all(c.get('bitwise', True) for c in d['cfgs']))
+PY
+for pl in "16,16,4" "16,16,8" "16,32,4" "16,32,8"; do
+  PHASES_PLAN=$pl timeout 300 python tools/experiments/phases.py ab/libmoa_phases.so 128,256,512 2>&1 | sed "s/^/$pl /"
+done | tee gpurun_out/r02_phases_w2.txt
