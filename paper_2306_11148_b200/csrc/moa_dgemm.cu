@@ -224,10 +224,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // on one SMSP and cap every thread at 168 registers (the 64 fp64 accumulators
 // alone need 128), so the producer becomes a full warpgroup that gives its
 // registers to the consumers with setmaxnreg: per SMSP 1 x 40 + 2 x 232 regs.
-// KS: k-slabs per ring stage (one barrier wait and one release per KS slabs). The
-// large tiles use 1; the latency tiles use 4, so tiny problems pay a quarter of the
-// per-slab synchronisation.
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int KS = 1>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct K1Traits {
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
   static constexpr int kNBoxW = BN / WARPS_N / 16;
@@ -251,10 +248,8 @@ struct K1Traits {
   static constexpr int kMA = BM / WARPS_M / 8;  // A atoms (8 rows each) per warp
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
-  static constexpr int kSubBytes = kABytes + kBBytes;  // one k-slab of A and B
-  static constexpr int kStageBytes = KS * kSubBytes;
+  static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8;  // + full/empty barriers
-  static_assert(kSubBytes % 1024 == 0 || KS == 1, "sub-stages stay 1024-B aligned (128B swizzle)");
   static_assert(BM == 8 * kMA * WARPS_M && (kMA == 1 || kMA == 2 || kMA == 4), "warp tile is 8, 16 or 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -264,7 +259,7 @@ struct K1Traits {
 // low-k partial of a split tile), else from +0: the loads are predicated off by
 // passing m = 0, so there is ONE copy of the slab loop in the kernel (a branch
 // between load_acc and acc_zero once cost 5.4% in register copies).
-template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES, int KS, int SUB_BYTES>
+template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
                                               int& stage, uint32_t& phase,
                                               double* __restrict__ C, int64_t m, int64_t p, int64_t ldc,
@@ -275,7 +270,7 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
   unsigned long long waited = 0, tw0 = 0;
   const bool ph = threadIdx.x == 0;
 #endif
-  for (int kt = k0; kt < k1; kt += KS) {
+  for (int kt = k0; kt < k1; ++kt) {
 #ifdef MOA_K1_PHASES
     if (ph) tw0 = gtime();
 #endif
@@ -288,15 +283,7 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
     }
 #endif
     const uint8_t* sa = sptr + stage * STAGE_BYTES;
-    if constexpr (KS == 1) {
-      mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
-    } else {
-#pragma unroll
-      for (int j = 0; j < KS; ++j)
-        if (kt + j < k1)  // (the piece's last stage may hold fewer slabs)
-          mma_slab(acc, sa + j * SUB_BYTES + wm * 8 * MA * kRowBytes, sa + j * SUB_BYTES + A_BYTES + wn * NBOX * kBoxBytes,
-                   f);
-    }
+    mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
     // WAR across proxies: these generic-proxy LDS reads must be ordered before the
     // producer's next TMA (async-proxy) write of this stage. The arrive's .release
     // alone does not do it (ptxas even hoists the arrive above the slab's last
@@ -388,14 +375,14 @@ struct StaticSched {
 // from the accumulator registers, to each peers.dst[d] at the same (row, col) —
 // NVLink peer stores into the other ranks' C_full, overlapping the remaining
 // tiles' DMMA work; stream-K head partials stay local.
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC, bool PEER, int KS = 1>
-__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, KS>::kThreads,
-                                  K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, KS>::kMinBlocks)
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC, bool PEER>
+__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads,
+                                  K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ flags,
                 unsigned int* __restrict__ issued, const __grid_constant__ PeerDst peers, int mode) {
-  using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, KS>;
+  using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
@@ -440,21 +427,18 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, KS>
         int64_t tm, tn;
         tile_coords(t, tiles_m, tiles_n, group, tm, tn);
         const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
-        for (int kt = k0; kt < k1; kt += KS) {
+        for (int kt = k0; kt < k1; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1u);
           const uint32_t fb = full0 + 8 * stage;
 #ifdef MOA_K1_PHASES
           if (kt == 0) MOA_PH(2, gtime());
 #endif
-          const int ns = KS == 1 ? 1 : (k1 - kt < KS ? k1 - kt : KS);  // slabs in this stage
-          mbar_arrive_expect_tx(fb, ns * Tr::kSubBytes);
-          for (int j = 0; j < ns; ++j) {
-            const uint32_t sa = sbase + stage * Tr::kStageBytes + j * Tr::kSubBytes;
-            tma_load_2d(sa, &tmA, fb, (kt + j) * kBK, row0);
+          mbar_arrive_expect_tx(fb, Tr::kStageBytes);
+          const uint32_t sa = sbase + stage * Tr::kStageBytes;
+          tma_load_2d(sa, &tmA, fb, kt * kBK, row0);
 #pragma unroll
-            for (int b = 0; b < BN / 16; ++b)
-              tma_load_2d(sa + Tr::kABytes + b * kBoxBytes, &tmB, fb, col0 + 16 * b, (kt + j) * kBK);
-          }
+          for (int b = 0; b < BN / 16; ++b)
+            tma_load_2d(sa + Tr::kABytes + b * kBoxBytes, &tmB, fb, col0 + 16 * b, kt * kBK);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -504,7 +488,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, KS>
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
-    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes, KS, Tr::kSubBytes>(
+    consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(
         acc, sptr, full0, empty0, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1, ACC || tail, f, lane);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
@@ -578,11 +562,11 @@ bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 // Opt in to the full dynamic smem per CTA and the maximum shared-memory carveout:
 // without the carveout the driver picked a smaller L1/smem split and the small
 // tiles fit fewer CTAs per SM than their smem allows (32x32x3: 6 instead of 8).
-template <int BM, int BN, int WM, int WN, int ST, bool ACC, bool PEER, int KS = 1>
+template <int BM, int BN, int WM, int WN, int ST, bool ACC, bool PEER>
 cudaError_t k1_attrs() {
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC, PEER, KS>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC, PEER>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       K1Traits<BM, BN, WM, WN, ST, KS>::kSmem);
+                                       K1Traits<BM, BN, WM, WN, ST>::kSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   return e;
 }
@@ -596,27 +580,27 @@ bool k1_wave_gate() {
   return on;
 }
 
-template <int BM, int BN, int WM, int WN, int ST, int KS = 1>
+template <int BM, int BN, int WM, int WN, int ST>
 int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
-  using Tr = K1Traits<BM, BN, WM, WN, ST, KS>;
+  using Tr = K1Traits<BM, BN, WM, WN, ST>;
   CUtensorMap ta, tb;
   const int64_t m = g.m, n = g.n, p = g.p;
   if (!encode_2d_f64(&ta, g.A, m, n, g.lda, BM) || !encode_2d_f64(&tb, g.B, n, p, g.ldb, 16)) return MOA_ERR_CUDA;
   double* C = (double*)g.C;
   const bool peer = g.peers && g.peers->nd > 0;
   auto kern = g.accumulate
-                  ? (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, true, true, KS> : k_dgemm_tma<BM, BN, WM, WN, ST, true, false, KS>)
-                  : (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, false, true, KS> : k_dgemm_tma<BM, BN, WM, WN, ST, false, false, KS>);
+                  ? (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, true, true> : k_dgemm_tma<BM, BN, WM, WN, ST, true, false>)
+                  : (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, false, true> : k_dgemm_tma<BM, BN, WM, WN, ST, false, false>);
   PeerDst peers{};
   if (peer) peers = *g.peers;
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     RelaxedCapture relaxed_capture;
-    attr_err = k1_attrs<BM, BN, WM, WN, ST, false, false, KS>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, false, KS>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, false, true, KS>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, true, KS>();
+    attr_err = k1_attrs<BM, BN, WM, WN, ST, false, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, false, true>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, true>();
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
@@ -687,11 +671,11 @@ TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
 };
 
-template <int BM, int BN, int WM, int WN, int ST, int KS = 1>
+template <int BM, int BN, int WM, int WN, int ST>
 int k1_occupancy() {
-  using Tr = K1Traits<BM, BN, WM, WN, ST, KS>;
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false, false, KS>;
-  if (k1_attrs<BM, BN, WM, WN, ST, false, false, KS>() != cudaSuccess) return 0;
+  using Tr = K1Traits<BM, BN, WM, WN, ST>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false, false>;
+  if (k1_attrs<BM, BN, WM, WN, ST, false, false>() != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Tr::kThreads, Tr::kSmem) != cudaSuccess) return 0;
   return n;
