@@ -91,6 +91,7 @@ def parse(argv=None):
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--sweep-sizes", default="1024,1536,2048,3072,4096,6144,8192,16000,16384")
     ap.add_argument("--sweep-windows", type=int, default=3)
+    ap.add_argument("--watchdog-s", type=float, default=1800.0, help="exit with stack dumps after this long (0: off)")
     return ap.parse_args(argv)
 
 
@@ -334,6 +335,11 @@ def main(argv=None):
     _quiet_stdout()
     argv = sys.argv[1:] if argv is None else argv
     args = parse(argv)
+    # Watchdog: a rank that stops making progress (a collective that never completes
+    # on a box this build could not test on) dumps its stacks and exits instead of
+    # holding the run; torchrun then stops the other ranks.
+    if args.watchdog_s > 0:
+        faulthandler.dump_traceback_later(args.watchdog_s, exit=True)
     if args.impl == "reference":
         return run_reference(args)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
