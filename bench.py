@@ -67,6 +67,7 @@ def workload_config(N, G, exchange="pull"):
     ex = {"pull": "copy-engine pulls of B's k-panels from rank 0's symmetric window over NVLink (moa_pull_panels), "
                   "overlapped with the k-panel chain of each rank's GEMM",
           "nccl": "NCCL broadcast of B in pipelined k-panels (moa_lift_panels) on a CTA-limited communicator",
+          "direct": "no copy of B: every rank's GEMM reads rank 0's window in place over NVLink (moa_gemm_lifted_direct)",
           "none": "none (one rank)"}[exchange if G > 1 else "none"]
     return {"workload": f"row-lifted fp64 GEMM m=n=p={N} on {G} B200 (BASELINE configs[4]), strong scaling: rank g "
                         f"owns rows moa_lift_rows({N}, {G}, g) of A and C; B ({N * N * 8 / 2 ** 30:.3g} GiB) travels "
@@ -84,7 +85,7 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["moa", "reference"], default="moa")
     ap.add_argument("--N", type=int, default=WORKLOAD_N, help="m = n = p (default: BASELINE configs[4], 32768)")
-    ap.add_argument("--exchange", choices=["pull", "nccl"], default="pull")
+    ap.add_argument("--exchange", choices=["pull", "nccl", "direct"], default="pull")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -382,7 +383,7 @@ def main(argv=None):
         I.device_fill(A, 1, I.ID_A, row0=row0)
 
     def make_B(kind):
-        Bt = comm.alloc_window((n, p)) if (kind == "pull" and G > 1) else torch.empty((n, p), dtype=torch.float64,
+        Bt = comm.alloc_window((n, p)) if (kind in ("pull", "direct") and G > 1) else torch.empty((n, p), dtype=torch.float64,
                                                                                     device=dev)
         if rank == 0:
             I.device_fill(Bt, 1, I.ID_B)
@@ -391,7 +392,7 @@ def main(argv=None):
         return Bt
 
     def free_B(Bt):
-        if G > 1 and Bt is not None and args.exchange == "pull" and Bt.data_ptr() in comm._windows:
+        if G > 1 and Bt is not None and args.exchange in ("pull", "direct") and Bt.data_ptr() in comm._windows:
             torch.cuda.synchronize()
             dist.barrier()
             comm.free_window(Bt)
@@ -401,8 +402,11 @@ def main(argv=None):
     B = make_B(exchange)
     B_hold = {}
 
-    def step(Bt):
-        moa.gemm_lifted(m, A, Bt, C, comm)
+    def step(Bt, kind=None):
+        if (kind or exchange) == "direct":
+            moa.gemm_lifted_direct(m, A, Bt, C, comm)
+        else:
+            moa.gemm_lifted(m, A, Bt, C, comm)
 
     def timed(fn, k):
         """k calls of fn between a barrier + synchronize on both sides; device time (ms)
@@ -481,7 +485,8 @@ def main(argv=None):
     if G > 1:
         A0 = torch.empty((0, n), dtype=torch.float64, device=dev)
         C0 = torch.empty((0, p), dtype=torch.float64, device=dev)
-        exch_ms, _ = timed(lambda: moa.gemm_lifted(0, A0, B, C0, comm), 3)
+        lifted0 = moa.gemm_lifted_direct if exchange == "direct" else moa.gemm_lifted
+        exch_ms, _ = timed(lambda: lifted0(0, A0, B, C0, comm), 3)
         exch_ms /= 3
     step_ms = elapsed_ms / args.steps
     kflops = 2.0 * rows * n * p
@@ -521,10 +526,10 @@ def main(argv=None):
         try:
             B_hold["other"] = make_B(other)
             Bo = B_hold["other"]
-            step(Bo)
+            step(Bo, other)
             torch.cuda.synchronize()
             k2 = max(2, min(args.steps, 5))
-            el2, _ = timed(lambda: step(Bo), k2)
+            el2, _ = timed(lambda: step(Bo, other), k2)
             variants[other] = {"ms_per_step": round(el2 / k2, 3), "gflops": round(flops_step * k2 / (el2 / 1e3) / 1e9, 1)}
             if other == "pull":
                 torch.cuda.synchronize()

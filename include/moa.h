@@ -184,6 +184,19 @@ int moa_gemm_lifted_host(int64_t m, int64_t n, int64_t p, const void* A_host, co
 int moa_gemm_lifted(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local, void* C_full,
                     int dtype, void* stream, moa_comm_t comm);
 
+/* moa_gemm_lifted_direct — row lifting with NO copy of B.
+ * COLLECTIVE. B must lie inside a window from moa_comm_alloc_window on every rank
+ * (only rank 0's copy is read; the others are never written). Every rank's K1
+ * producer streams B's k-slabs by TMA straight from rank 0's copy through this
+ * process's NVLink mapping of rank 0's window — the broadcast disappears into the
+ * GEMM's own loads. Entry barrier (rank 0's B is final), exit barrier (every read of
+ * it is complete); C_full as moa_gemm_lifted. Bitwise identical to moa_gemm. Peer
+ * reads do not stay in the reader's L2, so every tile row re-reads its B panel over
+ * NVLink: a design alternative to the pulled copy, not the default.
+ * Errors as moa_gemm_lifted; MOA_ERR_NOT_REGISTERED if B is not inside a window. */
+int moa_gemm_lifted_direct(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local,
+                           void* C_full, int dtype, void* stream, moa_comm_t comm);
+
 /* moa_gemm_lifted_ex — as moa_gemm_lifted with an explicit number of k-panels
  * (0 = the static choice moa_lift_panels). With npanels > 1 the broadcast of B
  * is pipelined: B's rows are split into npanels contiguous k-panels (each one
@@ -328,6 +341,7 @@ typedef enum {
 #define MOA_XF_GATHER 1       /* C_full given, gathered with NCCL (rows: all-gather / per-rank broadcasts; cols: via workspace) */
 #define MOA_XF_FUSED_GATHER 2 /* C_full inside a window: gather fused into the GEMM epilogue, entry/exit barriers */
 #define MOA_XF_PULL_B 4       /* rows: B inside a window on every rank: copy-engine pulls of B's k-panels from rank 0 */
+#define MOA_XF_DIRECT_B 8     /* rows: every rank's GEMM reads rank 0's B in place over NVLink (moa_gemm_lifted_direct) */
 typedef struct {
   int32_t op, comm, root, group, operand, phase, panel, reserved;
   int64_t offset, count;

@@ -22,6 +22,7 @@ from typing import Optional, Sequence
 __all__ = [
     "F64", "F32", "F32_3XTF32", "MoAError", "Plan", "gemm", "gemm_with_plan", "gemm_host", "gemm_lifted",
     "psi", "lift_rows", "plan", "select_block_paper", "Comm", "lib_path", "abi_version", "KERNEL_NAMES",
+    "gemm_lifted_direct",
     "gemm_acc", "lift_panels", "hadamard", "kron", "gemm_lifted_cols", "gemm_lifted_2d", "gemm_scatter",
     "gemm_lifted_gather", "gemm_lifted_host", "exchange_plan", "pull_panels", "Coll", "XPLAN_ROWS",
     "XPLAN_ROWS_HOST", "XPLAN_COLS", "XPLAN_2D", "XF_GATHER", "XF_FUSED_GATHER", "XF_PULL_B",
@@ -67,6 +68,7 @@ _moa_gemm_host = _sig("moa_gemm_host", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _v
 _moa_gemm_lifted_host = _sig("moa_gemm_lifted_host", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_lifted = _sig("moa_gemm_lifted", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_lifted_ex = _sig("moa_gemm_lifted_ex", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32])
+_moa_gemm_lifted_direct = _sig("moa_gemm_lifted_direct", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
 _moa_gemm_acc = _sig("moa_gemm_acc", [_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp])
 _moa_lift_panels = _sig("moa_lift_panels", [_i64, _i64, _i32, _i32])
 _moa_gemm_lifted_cols = _sig("moa_gemm_lifted_cols", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp])
@@ -149,7 +151,7 @@ def lift_panels(n: int, p: int, dtype: int = F64, nranks: int = 1) -> int:
 
 
 XPLAN_ROWS, XPLAN_ROWS_HOST, XPLAN_COLS, XPLAN_2D = 0, 1, 2, 3
-XF_GATHER, XF_FUSED_GATHER, XF_PULL_B = 1, 2, 4
+XF_GATHER, XF_FUSED_GATHER, XF_PULL_B, XF_DIRECT_B = 1, 2, 4, 8
 _COLL_OPS = {1: "broadcast", 2: "allgather", 3: "barrier", 4: "pull"}
 _COMM_KINDS = {0: "world", 1: "pipe", 2: "row", 3: "col"}
 _OPERANDS = {0: "A", 1: "B", 2: "C"}
@@ -521,6 +523,23 @@ def gemm_lifted(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, precisi
     _check(_moa_gemm_lifted_ex(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None,
                                C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
                                code, _stream_ptr(stream, B.get_device()), comm.handle, npanels), "moa_gemm_lifted_ex")
+    return C_local
+
+
+def gemm_lifted_direct(m: int, A_local, B, C_local, comm: Comm, C_full=None, *, stream=None):
+    """Row-lifted C := A • B with no copy of B (moa_gemm_lifted_direct; collective): B is
+    a comm.alloc_window tensor on every rank, and every rank's GEMM reads rank 0's copy
+    in place over NVLink."""
+    _arg(B, "B", (None, None), None)
+    n, p = B.shape
+    r0, rows = lift_rows(m, comm.world, comm.rank)
+    _arg(A_local, "A_local", (rows, n), B.dtype)
+    _arg(C_local, "C_local", (rows, p), B.dtype)
+    _arg(C_full, "C_full", (m, p), B.dtype, optional=True)
+    code = _code(B.dtype, None)
+    _check(_moa_gemm_lifted_direct(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None,
+                                   C_local.data_ptr() or None, None if C_full is None else (C_full.data_ptr() or None),
+                                   code, _stream_ptr(stream, B.get_device()), comm.handle), "moa_gemm_lifted_direct")
     return C_local
 
 

@@ -1042,15 +1042,17 @@ void build_plan(int variant, int64_t m, int64_t n, int64_t p, int dtype, int G, 
                 int grid_cols, int npanels, int flags, PlanOut* out) {
   if (G <= 1) return;  // nothing travels on a 1-rank communicator
   const bool fused = flags & MOA_XF_FUSED_GATHER, gather = (flags & MOA_XF_GATHER) && !fused,
-             pull = flags & MOA_XF_PULL_B;
+             direct = flags & MOA_XF_DIRECT_B, pull = (flags & MOA_XF_PULL_B) && !direct;
   int64_t bnd[kMaxPanels + 1];
   switch (variant) {
     case MOA_XPLAN_ROWS: {
       if (m * p == 0 && n * p == 0) return;
       // entry barrier: (fused) no rank stores into a peer's C_full before the peer
-      // reached this call; (pull) rank 0's B is final before anyone reads it
-      if (fused || pull) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 0, -1, 0, 1);
-      if (n * p > 0) {
+      // reached this call; (pull, direct) rank 0's B is final before anyone reads it
+      if (fused || pull || direct) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 0, -1, 0, 1);
+      // (direct: B never moves as a collective — every rank's GEMM reads rank 0's copy
+      // through its TMA loads over NVLink)
+      if (n * p > 0 && !direct) {
         if (pull) {
           // every processor reads all of B: ranks g > 0 pull it from rank 0
           if (rank != 0) {
@@ -1077,9 +1079,9 @@ void build_plan(int variant, int64_t m, int64_t n, int64_t p, int dtype, int G, 
           }
         }
       }
-      // exit barrier: (fused) every peer store is complete; (pull) every pull of
-      // rank 0's B is complete before rank 0 may change it
-      if (fused || pull) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 2, -1, 0, 1);
+      // exit barrier: (fused) every peer store is complete; (pull, direct) every read
+      // of rank 0's B is complete before rank 0 may change it
+      if (fused || pull || direct) out->add(MOA_COLL_BARRIER, MOA_COMM_WORLD, -1, 0, MOA_OPERAND_C, 2, -1, 0, 1);
       return;
     }
     case MOA_XPLAN_ROWS_HOST: {
@@ -1240,7 +1242,7 @@ static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const
                             int flags, const PeerDst* last_peers) {
   const int64_t es = elem_size(dtype);
   const int G = comm->nranks;
-  const bool pull = flags & MOA_XF_PULL_B;
+  const bool direct = flags & MOA_XF_DIRECT_B, pull = (flags & MOA_XF_PULL_B) && !direct;
   const std::vector<moa_coll_t> ops =
       plan_vec(MOA_XPLAN_ROWS, m, n, p, dtype, G, comm->rank, 0, 0, npanels, flags);
   // compute panels: the same boundaries as the plan's B ops (or one panel where no B
@@ -1249,13 +1251,20 @@ static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const
   int K;
   if (pull)
     K = (G > 1 && comm->rank != 0) ? moa_pull_panels(n, bnd) : (bnd[0] = 0, bnd[1] = n, 1);
+  else if (direct)
+    K = (bnd[0] = 0, bnd[1] = n, 1);
   else
     K = nccl_panel_bounds(n, npanels > 0 ? npanels : moa_lift_panels(n, p, dtype, G), bnd);
-  const moa_comm_s::Window* bwin = pull ? find_window(comm, B, n * p * es) : nullptr;
-  if (pull && n * p > 0 && !bwin) {
-    set_error("MOA_XF_PULL_B without B in a window");
+  const moa_comm_s::Window* bwin = (pull || direct) ? find_window(comm, B, n * p * es) : nullptr;
+  if ((pull || direct) && n * p > 0 && !bwin) {
+    set_error("B is not inside a window of the communicator");
     return MOA_ERR_NOT_REGISTERED;
   }
+  // direct: the GEMM's B operand is rank 0's copy, addressed through this process's
+  // mapping of rank 0's window (NVLink load/store); rank 0 reads its own
+  const void* Bsrc = B;
+  if (direct && n * p > 0 && G > 1 && comm->rank != 0)
+    Bsrc = (const char*)bwin->peer[0] + ((uintptr_t)B - (uintptr_t)bwin->ptr);
   cudaError_t e;
   int rc;
   Nvtx whole("moa lifted rows");
@@ -1301,7 +1310,7 @@ static int lifted_rows_exec(int64_t m, int64_t n, int64_t p, int64_t rows, const
     if (has[j] && (e = cudaStreamWaitEvent(s, comm->ev_panel[j], 0)) != cudaSuccess)
       return cuda_fail(e, "cudaStreamWaitEvent");
     if (k1 <= k0 && j > 0) continue;
-    GemmArgs g{rows, k1 - k0, p, (const char*)A_local + k0 * es, (const char*)B + k0 * p * es, C_local,
+    GemmArgs g{rows, k1 - k0, p, (const char*)A_local + k0 * es, (const char*)Bsrc + k0 * p * es, C_local,
                n > 0 ? n : 1, p > 0 ? p : 1, p > 0 ? p : 1, j > 0 ? 1 : 0};
     if (j == K - 1) g.peers = last_peers;  // the final panel writes the final C
     if ((rc = gemm_reserving(g, dtype, s, reserve_sms && j < K - 1 ? kPipeCTAs : 0))) return rc;
@@ -1374,6 +1383,39 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
   if (comm->nranks > 1 && n * p > 0 && find_window(comm, B, n * p * es)) flags |= MOA_XF_PULL_B;
   return lifted_rows_exec(m, n, p, rows, A_local, B, C_local, C_full, dtype, (cudaStream_t)stream, comm, npanels,
                           flags, nullptr);
+}
+
+int moa_gemm_lifted_direct(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_local,
+                           void* C_full, int dtype, void* stream, moa_comm_t comm) {
+  if (!comm) {
+    set_error("NULL communicator");
+    return MOA_ERR_NULL_POINTER;
+  }
+  if (m < 0) {
+    set_error("negative extent");
+    return MOA_ERR_INVALID_SHAPE;
+  }
+  int64_t row0 = 0, rows = 0;
+  int rc = moa_lift_rows(m, comm->nranks, comm->rank, &row0, &rows);
+  if (rc) return rc;
+  if ((rc = validate(rows, n, p, A_local, B, C_local, dtype))) return rc;
+  const int64_t es = elem_size(dtype);
+  if (n * p > 0 && !find_window(comm, B, n * p * es)) {
+    set_error("moa_gemm_lifted_direct: B must lie inside a window from moa_comm_alloc_window on every rank");
+    return MOA_ERR_NOT_REGISTERED;
+  }
+  if (C_full && (reinterpret_cast<uintptr_t>(C_full) % (uintptr_t)es) != 0) {
+    set_error("C_full not aligned to the element size");
+    return MOA_ERR_MISALIGNED;
+  }
+  if (C_full && (overlap_bytes(C_full, m * p * es, B, n * p * es) || overlap_bytes(C_full, m * p * es, A_local, rows * n * es) ||
+                 overlap_bytes(C_full, m * p * es, C_local, rows * p * es))) {
+    set_error("C_full overlaps another operand");
+    return MOA_ERR_ALIASING;
+  }
+  const int flags = (C_full ? MOA_XF_GATHER : 0) | MOA_XF_DIRECT_B;
+  return lifted_rows_exec(m, n, p, rows, A_local, B, C_local, C_full, dtype, (cudaStream_t)stream, comm, 0, flags,
+                          nullptr);
 }
 
 int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B_local, void* C_local, void* C_full,

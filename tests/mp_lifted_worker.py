@@ -64,17 +64,27 @@ def main():
         checks = {}
         try:
             dist.barrier()
-            if kind in ("rows", "rows_pull", "rows_fused", "rows_pull_fused", "rows_host"):
+            if kind in ("rows", "rows_pull", "rows_fused", "rows_pull_fused", "rows_host", "rows_direct"):
                 r0, rows = moa.lift_rows(m, world, rank)
                 A_local = t(Ah[r0:r0 + rows], dt)
-                pull = kind in ("rows_pull", "rows_pull_fused")
+                pull = kind in ("rows_pull", "rows_pull_fused", "rows_direct")
                 B = comm.alloc_window((n, p), dt) if pull else nan((n, p), dt)
                 if rank == 0:
                     B.copy_(t(Bh, dt))
                 else:
                     B.fill_(float("nan"))
                 torch.cuda.synchronize()
-                if kind in ("rows", "rows_pull"):
+                if kind == "rows_direct":
+                    # no copy of B: every rank's GEMM reads rank 0's window; the other
+                    # ranks' B windows stay NaN (checked below)
+                    C_local = nan((rows, p), dt)
+                    C_full = nan((m, p), dt) if case.get("gather") else None
+                    moa.gemm_lifted_direct(m, A_local, B, C_local, comm, C_full=C_full)
+                    torch.cuda.synchronize()
+                    checks["C_local"] = np.array_equal(C_local.cpu().numpy(), ref[r0:r0 + rows])
+                    if C_full is not None:
+                        checks["C_full"] = np.array_equal(C_full.cpu().numpy(), ref)
+                elif kind in ("rows", "rows_pull"):
                     C_local = nan((rows, p), dt)
                     C_full = nan((m, p), dt) if case.get("gather") else None
                     moa.gemm_lifted(m, A_local, B, C_local, comm, C_full=C_full, npanels=case.get("npanels", 0))
@@ -99,7 +109,10 @@ def main():
                     Ad, Cd = nan((rows, n), dt), nan((rows, p), dt)
                     moa.gemm_lifted_host(m, hA, hB, hC, Ad, B, Cd, comm)
                     checks["C_host"] = np.array_equal(hC.numpy(), ref[r0:r0 + rows])
-                checks["B"] = np.array_equal(B.cpu().numpy(), Bh)
+                if kind == "rows_direct":
+                    checks["B"] = np.array_equal(B.cpu().numpy(), Bh) if rank == 0 else bool(torch.isnan(B).all())
+                else:
+                    checks["B"] = np.array_equal(B.cpu().numpy(), Bh)
                 if pull:
                     dist.barrier()
                     comm.free_window(B)

@@ -48,3 +48,23 @@ def test_bench_self_launches_G_ranks(G, N, cuda_device):
     assert d["e2e"]["d2h_bytes_per_step"] == N * N * 8
     assert d["gpu_launches"] == 3 * (len(__import__("paper_2306_11148_b200").pull_panels(N)) - 1)
     assert d["sweep"] is None and d["cpu_baseline"] is None
+
+
+@pytest.mark.gpu
+def test_bench_direct_exchange(cuda_device):
+    """bench.py --exchange direct (NEXT-1 step 2: every rank's GEMM reads rank 0's B in
+    place): the line names the exchange and carries the pulled one beside it."""
+    if not os.path.exists(SHIM):
+        subprocess.check_call([sys.executable, os.path.join(ROOT, "tools", "build.py"), "shim"])
+    env = dict(os.environ)
+    env.update({"LD_PRELOAD": SHIM, "MOA_BENCH_SHARE_GPU": "1", "MOA_NCCL_SHIM_TIMEOUT": "120"})
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--N", "1024", "--steps", "3",
+                        "--warmup", "1", "--no-cpu", "--no-e2e", "--exchange", "direct"], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-4000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][-1])
+    assert "no copy of B" in d["config"]["exchange"] and d["gpu_launches"] == 3
+    assert set(d["exchange_variants"]) == {"direct", "pull"}, d["exchange_variants"]
+    assert d["value"] > 0

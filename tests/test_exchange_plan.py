@@ -94,6 +94,23 @@ def test_rows_pull_reads_B_once_per_rank(m, n, p, G):
             assert [o.panel for o in pulls] == list(range(len(pulls)))
 
 
+@pytest.mark.parametrize("m,n,p,G", [(4096, 4096, 4096, 8), (100, 64, 50, 3), (0, 64, 64, 2), (64, 64, 64, 1)])
+def test_rows_direct_moves_no_B(m, n, p, G):
+    """NEXT-1 step 2 (moa_gemm_lifted_direct): B never travels as a collective or a copy —
+    the plan is the entry and exit barrier around rank 0's window, identical on every
+    rank, plus the optional NCCL gather of C."""
+    for gather in (0, moa.XF_GATHER):
+        plans = _plans(moa.XPLAN_ROWS, m, n, p, G, flags=moa.XF_DIRECT_B | gather)
+        assert all(pl == plans[0] for pl in plans)
+        if G == 1 or (m * p == 0 and n * p == 0):
+            assert plans[0] == []
+            continue
+        assert not [o for o in plans[0] if o.operand == "B" or o.op == "pull"]
+        ops = [o.op for o in plans[0]]
+        assert ops[0] == "barrier" and ops[-1] == "barrier"
+        assert (len(ops) > 2) == bool(gather and m * p > 0)
+
+
 def test_pull_panels_geometric():
     for n in [0, 1, 31, 63, 64, 100, 512, 4096, 16384, 32768, 65536, 10 ** 6]:
         b = moa.pull_panels(n)

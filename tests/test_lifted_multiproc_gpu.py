@@ -37,6 +37,8 @@ CASES = {
         dict(name="rows_static_f32", kind="rows", m=256, n=128, p=192, npanels=2, dtype="f32"),
         dict(name="rows_pull", kind="rows_pull", m=300, n=256, p=200, gather=True),
         dict(name="rows_pull_f32", kind="rows_pull", m=130, n=512, p=96, dtype="f32"),
+        dict(name="rows_direct", kind="rows_direct", m=300, n=256, p=200, gather=True),
+        dict(name="rows_direct_f32", kind="rows_direct", m=130, n=96, p=96, dtype="f32"),
         dict(name="rows_fused", kind="rows_fused", m=301, n=96, p=200, npanels=2),
         dict(name="rows_pull_fused", kind="rows_pull_fused", m=300, n=128, p=200),
         dict(name="rows_host", kind="rows_host", m=600, n=512, p=256),
@@ -52,6 +54,7 @@ CASES = {
         dict(name="rows_zero_row_rank", kind="rows", m=2, n=64, p=96, gather=True),
         dict(name="rows_uneven_k2", kind="rows", m=301, n=128, p=72, npanels=2, gather=True),
         dict(name="rows_pull_uneven", kind="rows_pull", m=100, n=512, p=64, gather=True),
+        dict(name="rows_direct_uneven", kind="rows_direct", m=100, n=512, p=64),
         dict(name="rows_fused_uneven", kind="rows_fused", m=200, n=64, p=128),
         dict(name="cols_uneven", kind="cols", m=64, n=48, p=100, gather=True),
         dict(name="rows_host_uneven", kind="rows_host", m=301, n=512, p=96),
@@ -83,6 +86,7 @@ def _plan_for(moa, case, G, rank):
         "rows_pull": (moa.XPLAN_ROWS, moa.XF_PULL_B | (moa.XF_GATHER if case.get("gather") else 0)),
         "rows_fused": (moa.XPLAN_ROWS, moa.XF_FUSED_GATHER),
         "rows_pull_fused": (moa.XPLAN_ROWS, moa.XF_FUSED_GATHER | moa.XF_PULL_B),
+        "rows_direct": (moa.XPLAN_ROWS, moa.XF_DIRECT_B | (moa.XF_GATHER if case.get("gather") else 0)),
         "rows_host": (moa.XPLAN_ROWS_HOST, 0),
         "cols": (moa.XPLAN_COLS, moa.XF_GATHER if case.get("gather") else 0),
         "cols_fused": (moa.XPLAN_COLS, moa.XF_FUSED_GATHER),
