@@ -2,7 +2,7 @@
 gemm_with_plan, alternating configs over R rounds (CUDA events, ~0.3 s per sample),
 median TF/s per (shape, config); every config must give the same bits.
 
-    python tools/experiments/cfg_ab.py "m,n,p;..." "bm,bn,stages;..." [ROUNDS]
+    python tools/experiments/cfg_ab.py "m,n,p;..." "bm,bn,stages[,grid];..." [ROUNDS]
 """
 import json
 import os
@@ -31,7 +31,8 @@ for (m, n, p) in shapes:
     same = {}
     for r in range(rounds):
         for c in cfgs:
-            pl = moa.Plan(**{**base.__dict__, "bm": c[0], "bn": c[1], "stages": c[2], "grid": 0})
+            # an optional 4th entry caps the grid (moa_gemm_with_plan honours a smaller grid)
+            pl = moa.Plan(**{**base.__dict__, "bm": c[0], "bn": c[1], "stages": c[2], "grid": c[3] if len(c) > 3 else 0})
             f = lambda: moa.gemm_with_plan(A, B, C, pl)  # noqa: E731
             for _ in range(3):
                 f()
