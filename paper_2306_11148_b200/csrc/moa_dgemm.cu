@@ -224,19 +224,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 // on one SMSP and cap every thread at 168 registers (the 64 fp64 accumulators
 // alone need 128), so the producer becomes a full warpgroup that gives its
 // registers to the consumers with setmaxnreg: per SMSP 1 x 40 + 2 x 232 regs.
-//
-// GROUPS = 2 ("ping-pong"): two independent consumer groups of WARPS_M x WARPS_N
-// warps, each with its own S-stage ring, its own producer lane and its own static
-// schedule over BM x BN tiles (virtual CTA = blockIdx.x + g * gridDim.x), so the
-// groups cross tile boundaries at unrelated times and one group's DMMA work covers
-// the other's drain/store/refill. Per SM it is two 64x128 "CTAs" that share one
-// register pool (setmaxnreg), which two real CTAs of 5 warps could not (200
-// registers per thread: spills in the slab loop).
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, int GROUPS = 1>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct K1Traits {
-  static constexpr int kGroups = GROUPS;
-  static constexpr int kGroupWarps = WARPS_M * WARPS_N;
-  static constexpr int kConsumerWarps = WARPS_M * WARPS_N * GROUPS;
+  static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
   static constexpr int kNBoxW = BN / WARPS_N / 16;
   // Only the 32x64 warp tile (64 accumulators) needs the producer's registers.
   static constexpr int kProducerWarps = (kConsumerWarps >= 8 && kNBoxW == 4) ? 4 : 1;
@@ -259,8 +249,7 @@ struct K1Traits {
   static constexpr int kABytes = BM * kRowBytes;
   static constexpr int kBBytes = BN * kRowBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = 1024 /*align slack*/ + GROUPS * STAGES * (kStageBytes + 2 * 8);  // + full/empty barriers
-  static_assert(GROUPS == 1 || (GROUPS == 2 && kProducerWarps >= 2), "one producer warp per group");
+  static constexpr int kSmem = 1024 /*align slack*/ + STAGES * kStageBytes + 2 * STAGES * 8;  // + full/empty barriers
   static_assert(BM == 8 * kMA * WARPS_M && (kMA == 1 || kMA == 2 || kMA == 4), "warp tile is 8, 16 or 32 rows");
   static_assert(BN % (16 * WARPS_N) == 0, "warp tile is a whole number of 16-column boxes");
 };
@@ -386,29 +375,21 @@ struct StaticSched {
 // from the accumulator registers, to each peers.dst[d] at the same (row, col) —
 // NVLink peer stores into the other ranks' C_full, overlapping the remaining
 // tiles' DMMA work; stream-K head partials stay local.
-template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC, bool PEER, int GROUPS = 1>
-__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GROUPS>::kThreads,
-                                  K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GROUPS>::kMinBlocks)
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool ACC, bool PEER>
+__global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kThreads,
+                                  K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kMinBlocks)
     k_dgemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 double* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n, int group, unsigned int* __restrict__ flags,
-                unsigned int* __restrict__ issued, const __grid_constant__ PeerDst peers, int mode, int vgrid) {
-  using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GROUPS>;
+                unsigned int* __restrict__ issued, const __grid_constant__ PeerDst peers, int mode) {
+  using Tr = K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t sbase0 = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // this warp's consumer group (producer warp kConsumerWarps + g serves group g)
-  const int grp = GROUPS == 1 ? 0 : (warp < Tr::kConsumerWarps ? warp / Tr::kGroupWarps : warp - Tr::kConsumerWarps);
-  const uint32_t sbase = sbase0 + grp * STAGES * Tr::kStageBytes;
+  const uint32_t sbase = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
   const uint8_t* sptr = smem_raw + (sbase - raw);
-  const uint32_t full0 = sbase0 + GROUPS * STAGES * Tr::kStageBytes + grp * STAGES * 16;
+  const uint32_t full0 = sbase + STAGES * Tr::kStageBytes;
   const uint32_t empty0 = full0 + STAGES * 8;
-  // virtual CTA of this group (GROUPS = 1: the CTA); vgrid virtual CTAs in all
-  // (GROUPS = 1 reads gridDim.x, as before the groups existed: same code generation)
-  const int64_t vcta = GROUPS == 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x + (int64_t)grp * gridDim.x;
-  const int64_t VG = GROUPS == 1 ? (int64_t)gridDim.x : (int64_t)vgrid;
-  const bool active = GROUPS == 1 || (grp < GROUPS && vcta < VG);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (int)((n + kBK - 1) / kBK);
 #ifdef MOA_K1_PHASES
   if (threadIdx.x == 0) MOA_PH(0, gtime());
@@ -421,14 +402,11 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GRO
   // placed as this grid's SMs free up (signalling at the start let small CTAs of the
   // next grids pile onto busy SMs: N=512 went from 15 to 23 us).
   if (threadIdx.x == 0) {
-    const uint32_t bar0 = sbase0 + GROUPS * STAGES * Tr::kStageBytes;
 #pragma unroll
-    for (int g = 0; g < GROUPS; ++g)
-#pragma unroll
-      for (int s = 0; s < STAGES; ++s) {
-        mbar_init(bar0 + g * STAGES * 16 + 8 * s, 1);
-        mbar_init(bar0 + g * STAGES * 16 + STAGES * 8 + 8 * s, Tr::kGroupWarps);
-      }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, Tr::kConsumerWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -440,7 +418,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GRO
   if (warp >= Tr::kConsumerWarps) {
     // ----------------------------- producer ---------------------------------
     if constexpr (Tr::kSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Tr::kProducerRegs));
-    if (active && warp - Tr::kConsumerWarps < GROUPS && lane == 0) {
+    if (warp == Tr::kConsumerWarps && lane == 0) {
       prefetch_tmap(&tmA);
       prefetch_tmap(&tmB);
       int stage = 0;
@@ -467,14 +445,14 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GRO
           }
         }
       };
-      const int64_t tiles = tiles_m * tiles_n, G = VG;
+      const int64_t tiles = tiles_m * tiles_n, G = gridDim.x;
       // Wave gate: the tiles of wave t/G start only once every tile of the earlier
       // waves has had all its loads issued, so the CTAs of a wave walk k in step and
       // share each A/B k-slab through L2 instead of drifting apart over many waves
       // (which re-read the panels from DRAM). The last issue precedes the last
       // consume by the ring depth, so the gate opens inside the producer's lead.
       const bool gate = (mode & kK1WaveGate) && issued;
-      StaticSched sc(tiles, ktiles, G, vcta, flags != nullptr);
+      StaticSched sc(tiles, ktiles, G, blockIdx.x, flags != nullptr);
       int64_t t;
       int k0, k1, run;
       while (sc.next(t, k0, k1, run)) {
@@ -489,12 +467,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GRO
 
   // ------------------------------- consumers ---------------------------------
   if constexpr (Tr::kSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Tr::kConsumerRegs));
-  if (!active) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    return;
-  }
-  const int lw = GROUPS == 1 ? warp : warp % Tr::kGroupWarps;
-  const int wm = lw % WARPS_M, wn = lw / WARPS_M;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   FragOffsets f = make_offsets(lane);
   // Opaque copies: computed once, kept live. Without this ptxas rematerialised the
   // offsets (S2R tid + ~25 integer ops) in every slab.
@@ -504,7 +477,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GRO
   Acc<Tr::kMA, Tr::kNBox> acc;
   int stage = 0;
   uint32_t phase = 0;
-  StaticSched sc(tiles_m * tiles_n, ktiles, VG, vcta, flags != nullptr);
+  StaticSched sc(tiles_m * tiles_n, ktiles, gridDim.x, blockIdx.x, flags != nullptr);
   for (;;) {
     int64_t tm, tn;
     int k0, k1, run;
@@ -514,11 +487,11 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES, GRO
     // consumers' code generation, profiles/r02/ab_bisect*.jsonl)
     tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
-    if (tail) split_wait(flags + run, Tr::kGroupWarps, lane);
+    if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
     consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(
         acc, sptr, full0, empty0, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1, ACC || tail, f, lane);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
-    if (tail) split_release(flags + run, 2 * Tr::kGroupWarps, lane);
+    if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
     if constexpr (PEER) {
       if (!head)
         for (int d = 0; d < peers.nd; ++d)
@@ -589,11 +562,11 @@ bool encode_2d_f64(CUtensorMap* map, const void* base, int64_t rows, int64_t col
 // Opt in to the full dynamic smem per CTA and the maximum shared-memory carveout:
 // without the carveout the driver picked a smaller L1/smem split and the small
 // tiles fit fewer CTAs per SM than their smem allows (32x32x3: 6 instead of 8).
-template <int BM, int BN, int WM, int WN, int ST, bool ACC, bool PEER, int GR = 1>
+template <int BM, int BN, int WM, int WN, int ST, bool ACC, bool PEER>
 cudaError_t k1_attrs() {
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC, PEER, GR>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, ACC, PEER>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       K1Traits<BM, BN, WM, WN, ST, GR>::kSmem);
+                                       K1Traits<BM, BN, WM, WN, ST>::kSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   return e;
 }
@@ -607,28 +580,27 @@ bool k1_wave_gate() {
   return on;
 }
 
-template <int BM, int BN, int WM, int WN, int ST, int GR = 1>
+template <int BM, int BN, int WM, int WN, int ST>
 int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
-  using Tr = K1Traits<BM, BN, WM, WN, ST, GR>;
+  using Tr = K1Traits<BM, BN, WM, WN, ST>;
   CUtensorMap ta, tb;
   const int64_t m = g.m, n = g.n, p = g.p;
   if (!encode_2d_f64(&ta, g.A, m, n, g.lda, BM) || !encode_2d_f64(&tb, g.B, n, p, g.ldb, 16)) return MOA_ERR_CUDA;
   double* C = (double*)g.C;
   const bool peer = g.peers && g.peers->nd > 0;
-  auto kern = g.accumulate ? (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, true, true, GR>
-                                   : k_dgemm_tma<BM, BN, WM, WN, ST, true, false, GR>)
-                           : (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, false, true, GR>
-                                   : k_dgemm_tma<BM, BN, WM, WN, ST, false, false, GR>);
+  auto kern = g.accumulate
+                  ? (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, true, true> : k_dgemm_tma<BM, BN, WM, WN, ST, true, false>)
+                  : (peer ? k_dgemm_tma<BM, BN, WM, WN, ST, false, true> : k_dgemm_tma<BM, BN, WM, WN, ST, false, false>);
   PeerDst peers{};
   if (peer) peers = *g.peers;
   static std::once_flag once;  // per instantiation
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     RelaxedCapture relaxed_capture;
-    attr_err = k1_attrs<BM, BN, WM, WN, ST, false, false, GR>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, false, GR>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, false, true, GR>();
-    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, true, GR>();
+    attr_err = k1_attrs<BM, BN, WM, WN, ST, false, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, false>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, false, true>();
+    if (attr_err == cudaSuccess) attr_err = k1_attrs<BM, BN, WM, WN, ST, true, true>();
   });
   if (attr_err != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
@@ -646,20 +618,7 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     if (gate && first >= 2 * plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   }
   cudaLaunchConfig_t cfg = {};
-  // GROUPS > 1: plan.grid counts virtual CTAs (consumer groups); a real CTA carries
-  // GR of them, virtual CTA v on real CTA v mod R, so a grid of at most one per SM
-  // stays spread over the SMs
-  const int64_t vgrid = plan.grid;
-  int64_t rgrid = vgrid;
-  if (GR > 1) {
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
-      set_error("cudaDeviceGetAttribute(MultiProcessorCount)");
-      return MOA_ERR_CUDA;
-    }
-    if (vgrid > sms) rgrid = (vgrid + GR - 1) / GR;
-  }
-  cfg.gridDim = dim3((unsigned)rgrid);
+  cfg.gridDim = dim3((unsigned)plan.grid);
   cfg.blockDim = dim3(Tr::kThreads);
   cfg.dynamicSmemBytes = Tr::kSmem;
   cfg.stream = stream;
@@ -672,7 +631,7 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   int mode = 0;
   if (ctr && gate) mode |= kK1WaveGate;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, C, m, n, p, g.ldc, plan.tiles_m, plan.tiles_n,
-                                     (int)plan.raster_group, flags, ctr, peers, mode, (int)vgrid);
+                                     (int)plan.raster_group, flags, ctr, peers, mode);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_dgemm_tma launch: ") + cudaGetErrorString(e));
@@ -707,32 +666,29 @@ TileConfig kK1Configs[] = {
     // sub-partitions); 8 stages ("stages" also tells them apart in a plan)
     {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 8, K1Traits<16, 32, 2, 2, 8>::kThreads, 4, K1Traits<16, 32, 2, 2, 8>::kSmem, 0.0},
     {MOA_KERNEL_DGEMM_TMA, 16, 16, 16, 8, K1Traits<16, 16, 2, 1, 8>::kThreads, 8, K1Traits<16, 16, 2, 1, 8>::kSmem, 0.0},
-    // two ping-pong consumer groups of 64x128 tiles per CTA (K1Traits GROUPS); ctas/SM
-    // counts groups
-    {MOA_KERNEL_DGEMM_TMA, 64, 128, 16, 4, K1Traits<64, 128, 2, 2, 4, 2>::kThreads, 2, K1Traits<64, 128, 2, 2, 4, 2>::kSmem, 0.0},
 };
 TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
 };
 
-template <int BM, int BN, int WM, int WN, int ST, int GR = 1>
+template <int BM, int BN, int WM, int WN, int ST>
 int k1_occupancy() {
-  using Tr = K1Traits<BM, BN, WM, WN, ST, GR>;
-  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false, false, GR>;
-  if (k1_attrs<BM, BN, WM, WN, ST, false, false, GR>() != cudaSuccess) return 0;
+  using Tr = K1Traits<BM, BN, WM, WN, ST>;
+  auto kern = k_dgemm_tma<BM, BN, WM, WN, ST, false, false>;
+  if (k1_attrs<BM, BN, WM, WN, ST, false, false>() != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Tr::kThreads, Tr::kSmem) != cudaSuccess) return 0;
-  return n * GR;  // virtual CTAs (consumer groups) per SM
+  return n;
 }
 
 void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
     RelaxedCapture relaxed_capture;
-    int o[9] = {k1_occupancy<128, 128, 4, 2, 6>(),  k1_occupancy<128, 64, 4, 2, 4>(),  k1_occupancy<64, 64, 2, 4, 4>(),
+    int o[8] = {k1_occupancy<128, 128, 4, 2, 6>(),  k1_occupancy<128, 64, 4, 2, 4>(),  k1_occupancy<64, 64, 2, 4, 4>(),
                  k1_occupancy<64, 32, 2, 2, 4>(),    k1_occupancy<16, 32, 1, 2, 4>(),    k1_occupancy<16, 16, 1, 1, 4>(),
-                 k1_occupancy<16, 32, 2, 2, 8>(),    k1_occupancy<16, 16, 2, 1, 8>(),    k1_occupancy<64, 128, 2, 2, 4, 2>()};
-    for (int i = 0; i < 9; ++i)
+                 k1_occupancy<16, 32, 2, 2, 8>(),    k1_occupancy<16, 16, 2, 1, 8>()};
+    for (int i = 0; i < 8; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
@@ -766,7 +722,6 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
   if (plan.bm == 16 && plan.bn == 16 && plan.stages == 4) return launch_k1<16, 16, 1, 1, 4>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 32 && plan.stages == 8) return launch_k1<16, 32, 2, 2, 8>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 16 && plan.stages == 8) return launch_k1<16, 16, 2, 1, 8>(plan, g, stream);
-  if (plan.bm == 64 && plan.bn == 128 && plan.stages == 4) return launch_k1<64, 128, 2, 2, 4, 2>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }

@@ -27,9 +27,7 @@ EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255
 # every compiled K1 tile config (bm, bn, stages), incl. the latency tiles
 K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4),
               # latency tiles with 8x16 warp tiles (stages 8 tells them apart)
-              (16, 32, 8), (16, 16, 8),
-              # two ping-pong consumer groups of 64x128 tiles per CTA
-              (64, 128, 4)]
+              (16, 32, 8), (16, 16, 8)]
 
 
 def _moa():
