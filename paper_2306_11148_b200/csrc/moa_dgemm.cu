@@ -571,13 +571,19 @@ cudaError_t k1_attrs() {
   return e;
 }
 
-// The wave gate is on by default; MOA_K1_WAVE_GATE=0 turns it off (A/B experiments).
-bool k1_wave_gate() {
-  static const bool on = [] {
+// The wave gate pays where CTA drift would otherwise cost DRAM re-reads: launches of
+// many waves. Measured: 32768^3 (443 waves) DRAM 2.6 TB -> 418 GB, -15% J/GEMM, +0.2%
+// time; 16384^3 (110 waves) 72 -> 55 GB, -3.5% J, equal time; 8192^3 (27.7 waves) no
+// traffic change and 0.5% slower gated, shallow k (65536x512x512, 13.8 waves) 0.1-0.3%
+// slower gated (profiles/r02/wave_gate.jsonl, ab_gate_shallow.jsonl). So it is on from
+// kK1GateWaves whole-tile waves up. MOA_K1_WAVE_GATE=0 / =1 force it off / on (A/B).
+constexpr int64_t kK1GateWaves = 48;
+int k1_wave_gate_mode() {  // 0 off, 1 on, 2 by size
+  static const int mode = [] {
     const char* e = getenv("MOA_K1_WAVE_GATE");
-    return !(e && e[0] == '0');
+    return (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
   }();
-  return on;
+  return mode;
 }
 
 template <int BM, int BN, int WM, int WN, int ST>
@@ -609,13 +615,15 @@ int launch_k1(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
   // Schedule (see the kernel): whole tiles by static stride, plus stream-K runs when
   // the last wave is partial; a counter carries the wave gate's issue count.
   unsigned int *flags = nullptr, *ctr = nullptr;
-  const bool gate = k1_wave_gate();
+  const int gmode = k1_wave_gate_mode();
+  bool gate = false;
   if (plan.tiles > plan.grid) {
     const bool sk = use_stream_k(plan.tiles, plan.grid);
     if (sk && !acquire_split_flags((unsigned)plan.grid + 1, stream, &flags)) return MOA_ERR_CUDA;
     const int64_t first = sk ? sk_first_tile(plan.tiles, plan.grid) : plan.tiles;
     // the gate's issue counter, when there are at least two waves of whole tiles
-    if (gate && first >= 2 * plan.grid && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
+    gate = gmode == 1 ? first >= 2 * plan.grid : gmode == 2 && first >= kK1GateWaves * plan.grid;
+    if (gate && !acquire_tile_counter(stream, &ctr)) return MOA_ERR_CUDA;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)plan.grid);
