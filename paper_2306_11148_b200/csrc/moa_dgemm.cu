@@ -224,6 +224,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // on one SMSP and cap every thread at 168 registers (the 64 fp64 accumulators
 // alone need 128), so the producer becomes a full warpgroup that gives its
 // registers to the consumers with setmaxnreg: per SMSP 1 x 40 + 2 x 232 regs.
+constexpr int kK1OneShotGroup = 4;  // k-slabs per barrier of a one-shot latency tile
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct K1Traits {
   static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
@@ -233,6 +234,11 @@ struct K1Traits {
   // 32x16 warp tiles fit 2 CTAs/SM; the 1-2 warp latency tiles (<= 16 rows per
   // warp) are meant to pack many CTAs per SM
   static constexpr int kMinBlocks = kNBoxW >= 2 ? 1 : (BM / WARPS_M <= 16 ? 8 : 2);
+  // One-shot latency tiles: a 16-stage ring holds all of k <= 256 of a tile, so when a
+  // CTA owns exactly one tile the producer issues every load up front (one barrier per
+  // kK1OneShotGroup slabs) and nothing is ever released or refilled; the consumers run
+  // the whole k-chain with kK1OneShotGroup slabs between barrier waits.
+  static constexpr bool kOneShotCfg = BM * BN <= 32 * 32 && STAGES >= 16;
   static constexpr bool kSetMaxNReg = kProducerWarps == 4;
   static constexpr int kProducerRegs = 40;  // 40 + 2 x 232 per SMSP; also the CTA pool: 4 x 40 + 8 x 232 = 12 x 168
   static constexpr int kConsumerRegs = 232;
@@ -421,11 +427,37 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     if (warp == Tr::kConsumerWarps && lane == 0) {
       prefetch_tmap(&tmA);
       prefetch_tmap(&tmB);
+      if constexpr (Tr::kOneShotCfg) {
+        if (ktiles <= STAGES && tiles_m * tiles_n <= (int64_t)gridDim.x && !flags) {  // one-shot (see K1Traits)
+          if (blockIdx.x < tiles_m * tiles_n) {
+            int64_t tm, tn;
+            tile_coords32(blockIdx.x, tiles_m, tiles_n, group, tm, tn);
+            const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
+            for (int g = 0; g * kK1OneShotGroup < ktiles; ++g) {
+              const int k0 = g * kK1OneShotGroup, k1 = min(ktiles, k0 + kK1OneShotGroup);
+              const uint32_t fb = full0 + 8 * g;
+              mbar_arrive_expect_tx(fb, (k1 - k0) * Tr::kStageBytes);
+              for (int kt = k0; kt < k1; ++kt) {
+                const uint32_t sa = sbase + kt * Tr::kStageBytes;
+                tma_load_2d(sa, &tmA, fb, kt * kBK, row0);
+#pragma unroll
+                for (int b = 0; b < BN / 16; ++b)
+                  tma_load_2d(sa + Tr::kABytes + b * kBoxBytes, &tmB, fb, col0 + 16 * b, kt * kBK);
+              }
+            }
+          }
+          asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+          return;
+        }
+      }
       int stage = 0;
       uint32_t phase = 0;
       auto emit = [&](int64_t t, int k0, int k1, int run) {
         int64_t tm, tn;
-        tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+        if constexpr (BM * BN <= 32 * 32)
+          tile_coords32(t, tiles_m, tiles_n, group, tm, tn);
+        else
+          tile_coords(t, tiles_m, tiles_n, group, tm, tn);
         const int row0 = (int)(tm * BM), col0 = (int)(tn * BN);
         for (int kt = k0; kt < k1; ++kt) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1u);
@@ -475,6 +507,33 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
   for (int s = 0; s < 4; ++s) asm volatile("" : "+r"(f.a[s]));
   asm volatile("" : "+r"(f.b[0]), "+r"(f.b[1]));
   Acc<Tr::kMA, Tr::kNBox> acc;
+  if constexpr (Tr::kOneShotCfg) {
+    if (ktiles <= STAGES && tiles_m * tiles_n <= (int64_t)gridDim.x && !flags) {  // one-shot (see K1Traits)
+      if (blockIdx.x < tiles_m * tiles_n) {
+        int64_t tm, tn;
+        tile_coords32(blockIdx.x, tiles_m, tiles_n, group, tm, tn);
+        const int64_t r0 = tm * BM + wm * 8 * Tr::kMA, c0 = tn * BN + wn * Tr::kNBox * 16;
+        load_acc<Tr::kMA, Tr::kNBox, true>(acc, C, ACC ? m : 0, p, ldc, r0, c0, f);
+        for (int g = 0; g * kK1OneShotGroup < ktiles; ++g) {
+          mbar_wait(full0 + 8 * g, 0);
+#pragma unroll
+          for (int j = 0; j < kK1OneShotGroup; ++j) {
+            const int kt = g * kK1OneShotGroup + j;
+            if (kt < ktiles) {
+              const uint8_t* sa = sptr + kt * Tr::kStageBytes;
+              mma_slab(acc, sa + wm * 8 * Tr::kMA * kRowBytes, sa + Tr::kABytes + wn * Tr::kNBox * kBoxBytes, f);
+            }
+          }
+        }
+        store_acc<Tr::kMA, Tr::kNBox, true>(acc, C, m, p, ldc, r0, c0, f);
+        if constexpr (PEER)
+          for (int d = 0; d < peers.nd; ++d)
+            store_acc<Tr::kMA, Tr::kNBox, true>(acc, reinterpret_cast<double*>(peers.dst[d]), m, p, ldc, r0, c0, f);
+      }
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      return;
+    }
+  }
   int stage = 0;
   uint32_t phase = 0;
   StaticSched sc(tiles_m * tiles_n, ktiles, gridDim.x, blockIdx.x, flags != nullptr);
@@ -485,7 +544,10 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     if (!sc.next(t, k0, k1, run)) break;
     // (the 64-bit map: a 32-bit one was measured 0.6% slower at 8192^3 through the
     // consumers' code generation, profiles/r02/ab_bisect*.jsonl)
-    tile_coords(t, tiles_m, tiles_n, group, tm, tn);
+    if constexpr (BM * BN <= 32 * 32)  // latency tiles (moa_ptx.cuh tile_coords32)
+      tile_coords32(t, tiles_m, tiles_n, group, tm, tn);
+    else
+      tile_coords(t, tiles_m, tiles_n, group, tm, tn);
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
     consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(
@@ -674,6 +736,9 @@ TileConfig kK1Configs[] = {
     // sub-partitions); 8 stages ("stages" also tells them apart in a plan)
     {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 8, K1Traits<16, 32, 2, 2, 8>::kThreads, 4, K1Traits<16, 32, 2, 2, 8>::kSmem, 0.0},
     {MOA_KERNEL_DGEMM_TMA, 16, 16, 16, 8, K1Traits<16, 16, 2, 1, 8>::kThreads, 8, K1Traits<16, 16, 2, 1, 8>::kSmem, 0.0},
+    // their one-shot twins (16 stages: all of k <= 256 resident, no stage release)
+    {MOA_KERNEL_DGEMM_TMA, 16, 32, 16, 16, K1Traits<16, 32, 2, 2, 16>::kThreads, 2, K1Traits<16, 32, 2, 2, 16>::kSmem, 0.0},
+    {MOA_KERNEL_DGEMM_TMA, 16, 16, 16, 16, K1Traits<16, 16, 2, 1, 16>::kThreads, 3, K1Traits<16, 16, 2, 1, 16>::kSmem, 0.0},
 };
 TileConfig kK2Configs[] = {
     {MOA_KERNEL_DGEMM_GENERIC, 64, 64, 16, 1, 128, 4, (64 + 64) * kRowBytes, 0.5},
@@ -693,10 +758,11 @@ void refine_occupancy() {
   static std::once_flag once;
   std::call_once(once, [] {
     RelaxedCapture relaxed_capture;
-    int o[8] = {k1_occupancy<128, 128, 4, 2, 6>(),  k1_occupancy<128, 64, 4, 2, 4>(),  k1_occupancy<64, 64, 2, 4, 4>(),
+    int o[10] = {k1_occupancy<128, 128, 4, 2, 6>(),  k1_occupancy<128, 64, 4, 2, 4>(),  k1_occupancy<64, 64, 2, 4, 4>(),
                  k1_occupancy<64, 32, 2, 2, 4>(),    k1_occupancy<16, 32, 1, 2, 4>(),    k1_occupancy<16, 16, 1, 1, 4>(),
-                 k1_occupancy<16, 32, 2, 2, 8>(),    k1_occupancy<16, 16, 2, 1, 8>()};
-    for (int i = 0; i < 8; ++i)
+                 k1_occupancy<16, 32, 2, 2, 8>(),    k1_occupancy<16, 16, 2, 1, 8>(),    k1_occupancy<16, 32, 2, 2, 16>(),
+                 k1_occupancy<16, 16, 2, 1, 16>()};
+    for (int i = 0; i < 10; ++i)
       if (o[i] > 0) kK1Configs[i].ctas_per_sm = o[i];
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_dgemm_generic<64, 64, 2, 2>, 128, 0) == cudaSuccess && n > 0)
@@ -730,6 +796,8 @@ int launch_dgemm_tma(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t str
   if (plan.bm == 16 && plan.bn == 16 && plan.stages == 4) return launch_k1<16, 16, 1, 1, 4>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 32 && plan.stages == 8) return launch_k1<16, 32, 2, 2, 8>(plan, g, stream);
   if (plan.bm == 16 && plan.bn == 16 && plan.stages == 8) return launch_k1<16, 16, 2, 1, 8>(plan, g, stream);
+  if (plan.bm == 16 && plan.bn == 32 && plan.stages == 16) return launch_k1<16, 32, 2, 2, 16>(plan, g, stream);
+  if (plan.bm == 16 && plan.bn == 16 && plan.stages == 16) return launch_k1<16, 16, 2, 1, 16>(plan, g, stream);
   set_error("no compiled K1 instance for this plan");
   return MOA_ERR_INVALID_SHAPE;
 }

@@ -269,8 +269,33 @@ int choose(int kernel, int64_t m, int64_t n, int64_t p, const DeviceShape& ds, m
   // puts more SM sub-partitions on the short k-chains: 256^3 4.45 vs 5.18 us.)
   if (kernel == MOA_KERNEL_DGEMM_TMA && (double)m * (double)p < (double)ds.sms * 64.0 * 32.0) {
     const int64_t t16 = ((m + 15) / 16) * ((p + 15) / 16), t32 = ((m + 15) / 16) * ((p + 31) / 32);
-    const int want_bn = 4 * t16 <= 11LL * ds.sms ? 16 : 32;
-    const int want_st = (want_bn == 16 || t32 <= 2LL * ds.sms) ? 8 : 4;
+    int want_bn = 4 * t16 <= 11LL * ds.sms ? 16 : 32;
+    int want_st = (want_bn == 16 || t32 <= 2LL * ds.sms) ? 8 : 4;
+    // All of k in one 16-stage ring (n <= 256) and one tile per resident CTA: the
+    // one-shot twins of the 8x16-warp tiles (K1Traits::kOneShotCfg: every load issued up
+    // front, no stage release). Their time is the operand stream into the busiest SM
+    // (each CTA loads its (bm + bn) x n operands once, all at the start) followed by the
+    // k-chain, so between the two the one with fewer bytes into the busiest SM wins:
+    // ceil(tiles / SMs) x (bm + bn). Measured (profiles/r02/small_n_oneshot.json,
+    // graph-timed): N = 64 / 128 / 192 take 16x16 (1.84 / 2.52 / 2.86 us), N = 256 takes
+    // 16x32 (3.56 us; 16x16 4.25; the ring-fed tiles before: 4.42).
+    if (want_st == 8 && (n + 15) / 16 <= 16) {
+      auto slots = [&](int bn) -> int64_t {
+        for (int i = 0; i < nc; ++i)
+          if (cfgs[i].bm == 16 && cfgs[i].bn == bn && cfgs[i].stages == 16 && cfgs[i].smem_bytes <= ds.smem_optin)
+            return (int64_t)ds.sms * cfgs[i].ctas_per_sm;
+        return 0;
+      };
+      const bool ok16 = t16 <= slots(16), ok32 = t32 <= slots(32);
+      const int64_t b16 = (t16 + ds.sms - 1) / ds.sms * 32, b32 = (t32 + ds.sms - 1) / ds.sms * 48;
+      if (ok32 && (!ok16 || b32 < b16)) {
+        want_bn = 32;
+        want_st = 16;
+      } else if (ok16) {
+        want_bn = 16;
+        want_st = 16;
+      }
+    }
     for (int i = 0; i < nc; ++i)
       if (cfgs[i].bm == 16 && cfgs[i].bn == want_bn && cfgs[i].stages == want_st && cfgs[i].smem_bytes <= ds.smem_optin) {
         ruled = true;

@@ -144,6 +144,22 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t 
   tn = r / gm;
 }
 
+// The same map in 32-bit arithmetic, for K1's latency tiles (tiny problems: tile
+// counts far below 2^31), whose prologue sits on the critical path of a ~4 us launch:
+// three 64-bit divisions cost ~0.2 us there. (The large tiles keep the 64-bit map; a
+// 32-bit one was slower at 8192^3 through code generation.)
+__device__ __forceinline__ void tile_coords32(int64_t t64, int64_t tiles_m64, int64_t tiles_n, int group,
+                                              int64_t& tm, int64_t& tn) {
+  const uint32_t t = (uint32_t)t64, tiles_m = (uint32_t)tiles_m64;
+  const uint32_t per_group = (uint32_t)group * (uint32_t)tiles_n;
+  const uint32_t g = t / per_group;
+  const uint32_t first = g * (uint32_t)group;
+  const uint32_t rem = tiles_m - first;
+  const uint32_t gm = rem < (uint32_t)group ? rem : (uint32_t)group;
+  const uint32_t r = t - g * per_group;
+  tm = first + r % gm;
+  tn = r / gm;
+}
 
 }  // namespace ptx
 #endif  // __CUDACC__

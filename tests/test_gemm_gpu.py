@@ -27,7 +27,9 @@ EDGE = [1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255
 # every compiled K1 tile config (bm, bn, stages), incl. the latency tiles
 K1_CONFIGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4),
               # latency tiles with 8x16 warp tiles (stages 8 tells them apart)
-              (16, 32, 8), (16, 16, 8)]
+              (16, 32, 8), (16, 16, 8),
+              # their one-shot twins (16 stages: all of k <= 256 resident)
+              (16, 32, 16), (16, 16, 16)]
 
 
 def _moa():
@@ -192,7 +194,8 @@ def test_each_compiled_tile_config_bitwise(cuda_device):
 def test_latency_tiles_bitwise(cuda_device, shape):
     """Tiny problems (configs[0], 256^3): the chooser's latency tiles (16x16 of two 8x16
     warps up to 2.75 tiles per SM, then 16x32 of four 8x16 warps up to 2 per SM, then
-    16x32 of two 16x16 warps; one tile per CTA) give the fused ip.c bits, ragged edges
+    16x32 of two 16x16 warps; one tile per CTA; for n <= 256 the one-shot twins with all
+    of k resident, whichever streams fewer bytes into the busiest SM) give the fused ip.c bits, ragged edges
     included, and the literal ip.c within 1e-12 sqrt(n); every latency config does;
     a two-panel accumulate chain started from +0 is the same chain; the fused-gather
     epilogue writes the same bits to an extra destination."""
@@ -205,6 +208,13 @@ def test_latency_tiles_bitwise(cuda_device, shape):
     pl = moa.plan(m, n, p)
     t16, t32 = -(-m // 16) * -(-p // 16), -(-m // 16) * -(-p // 32)
     want = (16, 16, 8) if 4 * t16 <= 11 * pl.sms else ((16, 32, 8) if t32 <= 2 * pl.sms else (16, 32, 4))
+    if want[2] == 8 and -(-n // 16) <= 16:  # one-shot twins: all of k resident, one tile per CTA
+        ok16, ok32 = t16 <= 3 * pl.sms, t32 <= 2 * pl.sms  # 64 / 96 KiB of smem per CTA
+        b16, b32 = -(-t16 // pl.sms) * 32, -(-t32 // pl.sms) * 48
+        if ok32 and (not ok16 or b32 < b16):
+            want = (16, 32, 16)
+        elif ok16:
+            want = (16, 16, 16)
     assert (pl.bm, pl.bn, pl.stages) == want, pl
     assert pl.grid == pl.tiles
     got = moa.gemm(tA, tB).cpu().numpy()

@@ -21,7 +21,8 @@ from inputs import inputs as I  # noqa: E402
 
 PEAK = 37.0
 CFGS = [("dgemm_tma", 128, 128, 6), ("dgemm_tma", 128, 64, 4), ("dgemm_tma", 64, 64, 4), ("dgemm_tma", 64, 32, 4),
-        ("dgemm_tma", 16, 32, 4), ("dgemm_tma", 16, 16, 4), ("dgemm_tma", 16, 32, 8), ("dgemm_tma", 16, 16, 8)]
+        ("dgemm_tma", 16, 32, 4), ("dgemm_tma", 16, 16, 4), ("dgemm_tma", 16, 32, 8), ("dgemm_tma", 16, 16, 8),
+        ("dgemm_tma", 16, 32, 16), ("dgemm_tma", 16, 16, 16)]
 
 
 def time_fn(fn, reps):
