@@ -1,7 +1,8 @@
 """Small-shape runs of every kernel (K1 fp64 TMA, K2 generic, K3 FFMA, K3g, K4 3xTF32)
 for compute-sanitizer (memcheck / racecheck / synccheck), plus K1 in its stream-K
 (1920x1024x1920: 225 128x128 tiles on 148 CTAs), 64x32 stream-K over 3 CTAs/SM (2000x48x2000)
-and dynamic + stream-K (7040x16x7040) schedules."""
+and dynamic + stream-K (7040x16x7040) schedules, the one-shot latency tiles (n <= 256,
+also in accumulate mode) and a ring-fed latency tile."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -23,6 +24,22 @@ for (m, n, p) in [(1920, 1024, 1920), (2000, 48, 2000), (7040, 16, 7040)]:
     same = bool(np.all(C == O.ip(A, B, fused=True)))
     pl = moa.plan(m, n, p)
     print(m, n, p, "float64 K1", pl.bm, pl.bn, "tiles", pl.tiles, "grid", pl.grid, "bitwise" if same else "MISMATCH")
+    ok &= same
+# latency tiles: one-shot (n <= 256: 256^3 and 200x96x260 above) in accumulate mode as a
+# two-panel chain, and the ring-fed latency tile (n > 256)
+for (m, n, p, k0) in [(200, 96, 260, 48), (300, 512, 300, 0)]:
+    A = I.host_matrix(m, n, 5, I.ID_A); B = I.host_matrix(n, p, 5, I.ID_B)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = torch.zeros((m, p), dtype=torch.float64, device="cuda")
+    if k0:
+        moa.gemm_acc(Ad[:, :k0], Bd[:k0], C, True)
+        moa.gemm_acc(Ad[:, k0:], Bd[k0:], C, True)
+    else:
+        C = moa.gemm(Ad, Bd)
+    torch.cuda.synchronize()
+    pl = moa.plan(m, n, p)
+    same = bool(np.all(C.cpu().numpy() == O.ip(A, B, fused=True)))
+    print(m, n, p, "float64 latency tile", pl.bm, pl.bn, pl.stages, "acc chain" if k0 else "", "bitwise" if same else "MISMATCH")
     ok &= same
 # fused-gather epilogue (K1/K2 PEER): 3 extra destinations, stream-K and generic shapes
 for (m, n, p) in [(2000, 48, 2000), (130, 34, 66), (257, 33, 131)]:
