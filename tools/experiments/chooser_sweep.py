@@ -16,7 +16,8 @@ import paper_2306_11148_b200 as moa  # noqa: E402
 from inputs import inputs as I  # noqa: E402
 from small_n import time_graph  # noqa: E402
 
-CFGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4)]
+CFGS = [(128, 128, 6), (128, 64, 4), (64, 64, 4), (64, 32, 4), (16, 32, 4), (16, 16, 4), (16, 32, 8), (16, 16, 8),
+        (16, 32, 16), (16, 16, 16)]
 ms = [256, 2048, 16384, 1 << 17]
 ns = [64, 512, 4096]
 ps = [32, 96, 200, 512, 2048, 8192]
