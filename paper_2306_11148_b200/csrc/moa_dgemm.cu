@@ -266,7 +266,7 @@ struct K1Traits {
 // passing m = 0, so there is ONE copy of the slab loop in the kernel (a branch
 // between load_acc and acc_zero once cost 5.4% in register copies).
 template <int MA, int NBOX, int STAGES, int STAGE_BYTES, int A_BYTES>
-__device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t* sptr, uint32_t full0, uint32_t empty0,
+__device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, uint32_t a_s, uint32_t b_s, uint32_t full0, uint32_t empty0,
                                               int& stage, uint32_t& phase,
                                               double* __restrict__ C, int64_t m, int64_t p, int64_t ldc,
                                               int64_t row0, int64_t col0, int wm, int wn, int k0, int k1, bool load,
@@ -288,8 +288,13 @@ __device__ __forceinline__ void consume_piece(Acc<MA, NBOX>& acc, const uint8_t*
       if (kt == k0) MOA_PH(3, tw1);
     }
 #endif
-    const uint8_t* sa = sptr + stage * STAGE_BYTES;
-    mma_slab(acc, sa + wm * 8 * MA * kRowBytes, sa + A_BYTES + wn * NBOX * kBoxBytes, f);
+    // a_s / b_s: this warp's A rows and B boxes in stage 0 (shared-window addresses,
+    // computed once by the caller and kept opaque); without them ptxas re-derived the
+    // window base (S2R SR_CgaCtaId, S2R SR_TID.X and ~20 integer ops) at every slab, on
+    // the critical path between the stage wait and the first fragment loads
+    const uint32_t so = (uint32_t)stage * STAGE_BYTES;
+    mma_slab(acc, static_cast<const uint8_t*>(__cvta_shared_to_generic(a_s + so)),
+             static_cast<const uint8_t*>(__cvta_shared_to_generic(b_s + so)), f);
     // WAR across proxies: these generic-proxy LDS reads must be ordered before the
     // producer's next TMA (async-proxy) write of this stage. The arrive's .release
     // alone does not do it (ptxas even hoists the arrive above the slab's last
@@ -506,6 +511,8 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
 #pragma unroll
   for (int s = 0; s < 4; ++s) asm volatile("" : "+r"(f.a[s]));
   asm volatile("" : "+r"(f.b[0]), "+r"(f.b[1]));
+  uint32_t a_s = sbase + wm * 8 * Tr::kMA * kRowBytes, b_s = sbase + Tr::kABytes + wn * Tr::kNBox * kBoxBytes;
+  asm volatile("" : "+r"(a_s), "+r"(b_s));
   Acc<Tr::kMA, Tr::kNBox> acc;
   if constexpr (Tr::kOneShotCfg) {
     if (ktiles <= STAGES && tiles_m * tiles_n <= (int64_t)gridDim.x && !flags) {  // one-shot (see K1Traits)
@@ -551,7 +558,7 @@ __global__ void __launch_bounds__(K1Traits<BM, BN, WARPS_M, WARPS_N, STAGES>::kT
     const bool head = k1 < ktiles, tail = k0 > 0;  // stream-K split pieces
     if (tail) split_wait(flags + run, Tr::kConsumerWarps, lane);
     consume_piece<Tr::kMA, Tr::kNBox, STAGES, Tr::kStageBytes, Tr::kABytes>(
-        acc, sptr, full0, empty0, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1, ACC || tail, f, lane);
+        acc, a_s, b_s, full0, empty0, stage, phase, C, m, p, ldc, tm * BM, tn * BN, wm, wn, k0, k1, ACC || tail, f, lane);
     if (head) split_signal(flags + run + 1, lane);  // low-k partial of this tile -> run + 1
     if (tail) split_release(flags + run, 2 * Tr::kConsumerWarps, lane);
     if constexpr (PEER) {
