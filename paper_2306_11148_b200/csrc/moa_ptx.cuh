@@ -144,10 +144,11 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t 
   tn = r / gm;
 }
 
-// The same map in 32-bit arithmetic, for K1's latency tiles (tiny problems: tile
-// counts far below 2^31), whose prologue sits on the critical path of a ~4 us launch:
-// three 64-bit divisions cost ~0.2 us there. (The large tiles keep the 64-bit map; a
-// 32-bit one was slower at 8192^3 through code generation.)
+// The same map in 32-bit arithmetic, for K1's latency tiles, whose prologue sits on
+// the critical path of a few-us launch (three 64-bit divisions: ~0.05-0.1 us of it,
+// profiles/r02/small_n_oneshot.json). Their tile count stays below 2^32 for any C that
+// fits in memory (2^32 tiles of 16x16 doubles would be 8 TiB). (The large tiles keep
+// the 64-bit map; a 32-bit one was slower at 8192^3 through code generation.)
 __device__ __forceinline__ void tile_coords32(int64_t t64, int64_t tiles_m64, int64_t tiles_n, int group,
                                               int64_t& tm, int64_t& tn) {
   const uint32_t t = (uint32_t)t64, tiles_m = (uint32_t)tiles_m64;
