@@ -219,8 +219,8 @@ int moa_gemm_lifted_ex(int64_t m, int64_t n, int64_t p, const void* A_local, voi
  *   C_local : device, m x cols_g, receives rank g's column block of C.
  *   C_full  : NULL, or device m x p receiving all of C on every rank; then
  *   workspace must hold m * ceil(p / G) elements (not needed when G == 1).
- *   If C_full lies inside a window from moa_comm_alloc_window and dtype is
- *   MOA_F64 or MOA_F32, the gather is fused into the GEMM epilogue instead (each rank's
+ *   If C_full lies inside a window from moa_comm_alloc_window (any dtype), the gather
+ *   is fused into the GEMM epilogue instead (each rank's
  *   column block is computed into its columns of C_full, row stride p, and stored
  *   by the same epilogue into every peer's C_full; entry/exit barriers as in
  *   moa_gemm_lifted_gather); workspace is then unused.
@@ -247,7 +247,8 @@ int moa_gemm_lifted_2d(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_
  * all of C on every rank. Rank (r, c) computes its block straight into C_full at
  * rows [row0_r, row0_r + rows_r) x columns [col0_c, col0_c + cols_c) (row stride p);
  * the same epilogue stores it into every other rank's C_full; C_block also receives
- * the block. Entry/exit barriers as moa_gemm_lifted_gather. MOA_F64 or MOA_F32. */
+ * the block. Entry/exit barriers as moa_gemm_lifted_gather. Any dtype (the 3xTF32 kernel
+ * carries the same epilogue). */
 int moa_gemm_lifted_2d_gather(int64_t m, int64_t n, int64_t p, int grid_rows, int grid_cols, void* A_panel,
                               void* B_panel, void* C_block, void* C_full, int dtype, void* stream, moa_comm_t comm);
 
@@ -267,8 +268,9 @@ int moa_gemm_lifted_2d_gather(int64_t m, int64_t n, int64_t p, int grid_rows, in
  * dst[0..ndst): each an m x p row-major block with row stride ldc (DEVICE address;
  * may be a peer GPU's memory mapped into this process, e.g. from
  * moa_comm_window_peer). Every destination receives exactly the bits of C. With
- * accumulate != 0 (the last k-panel of a chain) only C is read. MOA_F64 or
- * MOA_F32 (the exact kernels; MOA_ERR_INVALID_DTYPE otherwise); 0 <= ndst <= 8 (MOA_ERR_INVALID_SHAPE); destinations
+ * accumulate != 0 (the last k-panel of a chain) only C is read. Any dtype: every kernel
+ * carries the epilogue (for MOA_F32_3XTF32 the destinations receive exactly the bits of
+ * C, which is within that variant's tolerance); 0 <= ndst <= 8 (MOA_ERR_INVALID_SHAPE); destinations
  * non-NULL when m*p > 0, aligned to the element size (MOA_ERR_MISALIGNED otherwise),
  * and disjoint from A, B, C and each other (MOA_ERR_ALIASING). A destination that is
  * not 16-byte aligned routes the call to the generic kernel (same bits; the TMA
@@ -299,7 +301,9 @@ int moa_comm_window_peer(moa_comm_t comm, const void* ptr, int peer, void** out)
  *            rank's C_full holds all of C, bitwise equal to moa_gemm on one GPU.
  * Stream order: a one-element all-reduce barrier before the GEMM (no rank stores
  * into a peer's C_full before that peer reached this call) and one after it (all
- * peer stores are complete). MOA_F64 or MOA_F32; at most 9 ranks (one NVLink node). */
+ * peer stores are complete). Any dtype (for MOA_F32_3XTF32 with npanels > 1 the panel
+ * sums are added in the epilogue, so C_full agrees with moa_gemm within that variant's
+ * tolerance rather than bitwise); at most 9 ranks (one NVLink node). */
 int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local, void* B, void* C_full, int dtype,
                            void* stream, moa_comm_t comm, int npanels);
 

@@ -564,7 +564,8 @@ def gemm_lifted_host(m: int, A_host, B_host, C_host, A_dev, B_dev, C_dev, comm: 
     return C_host
 
 
-def gemm_lifted_gather(m: int, A_local, B, C_full, comm: Comm, *, stream=None, npanels: int = 0):
+def gemm_lifted_gather(m: int, A_local, B, C_full, comm: Comm, *, precision: Optional[str] = None, stream=None,
+                       npanels: int = 0):
     """Row-lifted C := A • B with the all-gather of C fused into the GEMM epilogue
     (moa_gemm_lifted_gather; collective). C_full (m x p) must come from
     comm.alloc_window; on return (stream order) it holds all of C on every rank."""
@@ -574,16 +575,17 @@ def gemm_lifted_gather(m: int, A_local, B, C_full, comm: Comm, *, stream=None, n
     _arg(A_local, "A_local", (rows, n), B.dtype)
     _arg(C_full, "C_full", (m, p), B.dtype)
     _check(_moa_gemm_lifted_gather(m, n, p, A_local.data_ptr() or None, B.data_ptr() or None,
-                                   C_full.data_ptr() or None, _code(B.dtype, None), _stream_ptr(stream, B.get_device()),
+                                   C_full.data_ptr() or None, _code(B.dtype, precision), _stream_ptr(stream, B.get_device()),
                                    comm.handle, npanels), "moa_gemm_lifted_gather")
     return C_full
 
 
-def gemm_scatter(A, B, out, dsts, *, accumulate: bool = False, stream=None):
+def gemm_scatter(A, B, out, dsts, *, accumulate: bool = False, precision: Optional[str] = None, stream=None):
     """C (+)= A • B (moa_gemm_acc semantics) whose epilogue also writes every final C
     tile to each tensor (or raw device address) in `dsts` — the fused-gather epilogue
     on one GPU (moa_gemm_scatter). A and B may be row-strided 2-D views (e.g. a
-    k-panel A[:, k0:k1], B[k0:k1, :]); out and every dst tensor are m x p contiguous."""
+    k-panel A[:, k0:k1], B[k0:k1, :]); out and every dst tensor are m x p contiguous.
+    precision='3xtf32' (float32) runs the tcgen05 variant with the same epilogue."""
     _arg(A, "A", (None, None), None, layout="rows")
     m, n = A.shape
     _arg(B, "B", (n, None), A.dtype, layout="rows")
@@ -598,7 +600,7 @@ def gemm_scatter(A, B, out, dsts, *, accumulate: bool = False, stream=None):
     arr = (_vp * max(1, len(addrs)))(*[a or None for a in addrs])
     _check(_moa_gemm_scatter(m, n, p, A.data_ptr() or None, _ld(A), B.data_ptr() or None, _ld(B),
                              out.data_ptr() or None, max(1, p), 1 if accumulate else 0, len(addrs), arr,
-                             _code(A.dtype, None), _stream_ptr(stream, A.get_device())), "moa_gemm_scatter")
+                             _code(A.dtype, precision), _stream_ptr(stream, A.get_device())), "moa_gemm_scatter")
     return out
 
 

@@ -444,10 +444,6 @@ int gemm_impl(const GemmArgs& g, int dtype, const moa_plan_t* plan, cudaStream_t
   Nvtx range("moa gemm");
   int rc = validate_g(g, dtype);
   if (rc) return rc;
-  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
-    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 and MOA_F32 only");
-    return MOA_ERR_INVALID_DTYPE;
-  }
   DeviceShape ds;
   if ((rc = get_device_shape(-1, &ds))) return rc;
   if ((rc = check_device(ds))) return rc;
@@ -991,10 +987,6 @@ int moa_pull_panels(int64_t n, int64_t* bnd) {
 static int gemm_reserving(const GemmArgs& g, int dtype, cudaStream_t s, int reserve) {
   int rc = validate_g(g, dtype);
   if (rc) return rc;
-  if (g.peers && g.peers->nd > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
-    set_error("extra C destinations (fused gather epilogue) are implemented for MOA_F64 and MOA_F32 only");
-    return MOA_ERR_INVALID_DTYPE;
-  }
   DeviceShape ds;
   if ((rc = get_device_shape(-1, &ds)) || (rc = check_device(ds))) return rc;
   moa_plan_t pl;
@@ -1465,12 +1457,12 @@ int moa_gemm_lifted_cols(int64_t m, int64_t n, int64_t p, void* A, const void* B
   if (rc) return rc;
   if ((rc = validate(m, n, cols, A, B_local, C_local, dtype))) return rc;
   const int64_t es = elem_size(dtype);
-  // C_full inside a symmetric window (moa_comm_alloc_window), fp64/fp32: the gather is
+  // C_full inside a symmetric window (moa_comm_alloc_window), any dtype: the gather is
   // fused into the GEMM epilogue — this rank's column block is computed straight into
   // its columns of C_full (row stride p) and stored by the same epilogue into every
   // peer's C_full over NVLink; no workspace, no per-rank broadcasts of C.
   const moa_comm_s::Window* win =
-      (C_full && m * p > 0 && (dtype == MOA_F64 || dtype == MOA_F32) && G - 1 <= kMaxPeerDst)
+      (C_full && m * p > 0 && G - 1 <= kMaxPeerDst)
           ? find_window(comm, C_full, m * p * es)
           : nullptr;
   if (C_full && m * p > 0 && !win) {
@@ -1548,10 +1540,6 @@ static int lifted_2d_impl(int64_t m, int64_t n, int64_t p, int grid_rows, int gr
   const int64_t es = elem_size(dtype);
   const moa_comm_s::Window* win = nullptr;
   if (C_full && m * p > 0) {  // the fused gather: C_full must be a symmetric window
-    if (dtype != MOA_F64 && dtype != MOA_F32) {
-      set_error("moa_gemm_lifted_2d_gather: MOA_F64 or MOA_F32 only");
-      return MOA_ERR_INVALID_DTYPE;
-    }
     if (comm->nranks - 1 > kMaxPeerDst) {
       set_error("moa_gemm_lifted_2d_gather: at most 9 ranks (one NVLink node)");
       return MOA_ERR_INVALID_SHAPE;
@@ -1643,10 +1631,6 @@ int moa_gemm_scatter(int64_t m, int64_t n, int64_t p, const void* A, int64_t lda
   GemmArgs g{m, n, p, A, B, C, lda, ldb, ldc, accumulate ? 1 : 0};
   int rc = validate_g(g, dtype);
   if (rc) return rc;
-  if (ndst > 0 && dtype != MOA_F64 && dtype != MOA_F32) {
-    set_error("moa_gemm_scatter: MOA_F64 or MOA_F32 only");
-    return MOA_ERR_INVALID_DTYPE;
-  }
   const int64_t es = elem_size(dtype);
   if (ndst > 0 && m * p > 0 && !dst) {
     set_error("NULL dst array");
@@ -1790,10 +1774,6 @@ int moa_gemm_lifted_gather(int64_t m, int64_t n, int64_t p, const void* A_local,
   if (npanels < 0 || npanels > kMaxPanels) {
     set_error("npanels out of range");
     return MOA_ERR_INVALID_SHAPE;
-  }
-  if (dtype != MOA_F64 && dtype != MOA_F32) {
-    set_error("moa_gemm_lifted_gather: MOA_F64 or MOA_F32 only");
-    return MOA_ERR_INVALID_DTYPE;
   }
   if (comm->nranks - 1 > kMaxPeerDst) {
     set_error("moa_gemm_lifted_gather: at most 9 ranks (one NVLink node)");

@@ -22,7 +22,9 @@
 //   warp 1      TMEM allocator + MMA issuer (one thread): per k-step of 8,
 //               3 x tcgen05.mma (M=128, N=BN, K=8) into a TMEM accumulator;
 //               tcgen05.commit frees the stage / publishes the finished tile.
-//   warps 6..9  epilogue: tcgen05.ld 32x32b -> registers -> global (row-major C).
+//   warps 6..9  epilogue: tcgen05.ld 32x32b -> registers -> global (row-major C), and
+//               the same bits to up to 8 further destinations (the fused-gather
+//               epilogue of moa_gemm_scatter / moa_gemm_lifted_gather, as K1/K3).
 // Accumulators are double-buffered in TMEM (2 x BN columns).
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -112,7 +114,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_3xtf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate,
-                   int64_t tiles_m, int64_t tiles_n, int group) {
+                   int64_t tiles_m, int64_t tiles_n, int group, const __grid_constant__ PeerDst peers) {
   using Tr = K4Traits<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw0 = smem_u32(smem_raw);
@@ -270,6 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
               }
               *reinterpret_cast<float4*>(dst + 4 * q) = v;
+              // the fused-gather epilogue (as K1/K3 PEER): the same bits to every extra
+              // destination, e.g. the other ranks' C_full over NVLink
+              for (int d = 0; d < peers.nd; ++d)
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(peers.dst[d]) + row * ldc + col + 4 * q) = v;
             }
         }
       }
@@ -333,7 +339,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_sgemm_3xtf32_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       float* __restrict__ C, int64_t m, int64_t n, int64_t p, int64_t ldc, int accumulate,
-                      int64_t tiles_m, int64_t tiles_n, int group) {
+                      int64_t tiles_m, int64_t tiles_n, int group, const __grid_constant__ PeerDst peers) {
   using Tr = K4TSTraits<BN, STAGES>;
   constexpr int NB = Tr::kAccBufs;
   extern __shared__ uint8_t smem_raw[];
@@ -506,6 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
               }
               *reinterpret_cast<float4*>(dst + 4 * q) = v;
+              for (int d = 0; d < peers.nd; ++d)  // fused-gather epilogue (see above)
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(peers.dst[d]) + row * ldc + col + 4 * q) = v;
             }
         }
       }
@@ -546,8 +554,10 @@ int launch_k4ts(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) 
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
+  PeerDst peers{};
+  if (g.peers) peers = *g.peers;
   kern<<<plan.grid, kThreads, Tr::kSmem, stream>>>(ta, tb, (float*)g.C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
-                                                   plan.tiles_n, plan.raster_group);
+                                                   plan.tiles_n, plan.raster_group, peers);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_3xtf32_ts launch: ") + cudaGetErrorString(e));
@@ -588,8 +598,10 @@ int launch_k4(const moa_plan_t& plan, const GemmArgs& g, cudaStream_t stream) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
     return MOA_ERR_CUDA;
   }
+  PeerDst peers{};
+  if (g.peers) peers = *g.peers;
   kern<<<plan.grid, kThreads, Tr::kSmem, stream>>>(ta, tb, C, m, n, p, g.ldc, g.accumulate, plan.tiles_m,
-                                                   plan.tiles_n, plan.raster_group);
+                                                   plan.tiles_n, plan.raster_group, peers);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_sgemm_3xtf32 launch: ") + cudaGetErrorString(e));

@@ -33,7 +33,7 @@ def test_scatter_validation_without_gpu():
     f = moa._moa_gemm_scatter
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 9, arr, 0, None) == 1            # ndst > 8
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, -1, arr, 0, None) == 1           # ndst < 0
-    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, arr, 2, None) == 2            # 3xTF32 + destinations
+    assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, arr, 3, None) == 2            # unknown dtype
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 1, None, 0, None) == 3           # NULL dst array
     bad = (moa._vp * 2)(D, None)
     assert f(4, 8, 8, A, 8, B, 8, C, 8, 0, 2, bad, 0, None) == 3            # NULL destination
@@ -141,13 +141,41 @@ def test_scatter_fp32_exact_bitwise(cuda_device, shape):
 
 
 @pytest.mark.gpu
-def test_scatter_rejects_3xtf32(cuda_device):
-    A = torch.ones((64, 64), dtype=torch.float32, device=cuda_device)
-    C = torch.empty((64, 64), dtype=torch.float32, device=cuda_device)
-    d = torch.empty((64, 64), dtype=torch.float32, device=cuda_device)
-    arr = (moa._vp * 1)(d.data_ptr())
-    rc = moa._moa_gemm_scatter(64, 64, 64, A.data_ptr(), 64, A.data_ptr(), 64, C.data_ptr(), 64, 0, 1, arr, 2, None)
-    assert rc == 2  # MOA_ERR_INVALID_DTYPE: the tcgen05 variant has no gather epilogue
+@pytest.mark.parametrize("shape", [(512, 256, 384), (300, 200, 260), (129, 33, 131)])
+def test_scatter_3xtf32(cuda_device, shape):
+    """The 3xTF32 tcgen05 kernel (K4) carries the fused-gather epilogue too: every
+    destination holds exactly the bits of C, C is within the variant's tolerance of the
+    literal oracle (5e-3, north_star) and at fp32 level vs the fp64 truth; a two-panel
+    accumulate chain scatters its final sums. (129x33x131 is not TMA-describable: the
+    exact fp32 generic kernel takes it, reading R20.)"""
+    m, n, p = shape
+    A = I.host_matrix(m, n, 7, I.ID_A, I.UNIFORM, np.float32)
+    B = I.host_matrix(n, p, 7, I.ID_B, I.UNIFORM, np.float32)
+    tA, tB = torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device)
+    if (m, n, p) != (129, 33, 131):
+        assert moa.plan(m, n, p, moa.F32_3XTF32).kernel == "sgemm_3xtf32"
+    C = torch.empty((m, p), dtype=torch.float32, device=cuda_device)
+    dst = [torch.full((m, p), float("nan"), dtype=torch.float32, device=cuda_device) for _ in range(3)]
+    moa.gemm_scatter(tA, tB, C, dst, precision="3xtf32")
+    torch.cuda.synchronize()
+    for t in dst:
+        assert torch.equal(t, C)
+    lit = O.ip(A, B, fused=False)
+    got = C.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(got - lit) <= 5e-3 * np.linalg.norm(lit)
+    truth = O.ip_f32_truth(A, B)
+    assert np.linalg.norm(got - truth) <= 1e-5 * np.sqrt(n) * np.linalg.norm(truth)
+    k0 = (n // 2) // 8 * 8 or n
+    C2 = torch.zeros((m, p), dtype=torch.float32, device=cuda_device)
+    d2 = torch.full((m, p), float("nan"), dtype=torch.float32, device=cuda_device)
+    moa.gemm_acc(tA[:, :k0], tB[:k0], C2, True, precision="3xtf32")
+    if k0 < n:
+        moa.gemm_scatter(tA[:, k0:], tB[k0:], C2, [d2], accumulate=True, precision="3xtf32")
+    else:
+        moa.gemm_scatter(tA[:, :0], tB[:0], C2, [d2], accumulate=True, precision="3xtf32")
+    torch.cuda.synchronize()
+    assert torch.equal(d2, C2)
+    assert np.linalg.norm(C2.cpu().numpy().astype(np.float64) - truth) <= 1e-5 * np.sqrt(n) * np.linalg.norm(truth)
 
 
 def _free_port():

@@ -49,6 +49,8 @@ CASES = {
         dict(name="grid_1x2", kind="2d", m=130, n=64, p=200, grid=[1, 2]),
         dict(name="grid_2x1", kind="2d", m=130, n=64, p=200, grid=[2, 1]),
         dict(name="grid_1x2_fused", kind="2d_fused", m=130, n=64, p=200, grid=[1, 2]),
+        # the 3xTF32 tcgen05 kernel's fused-gather epilogue (tolerance, not bits: reading R20's variant)
+        dict(name="rows_fused_3xtf32", kind="rows_fused", m=300, n=96, p=200, npanels=2, dtype="3xtf32"),
     ],
     3: [
         dict(name="rows_zero_row_rank", kind="rows", m=2, n=64, p=96, gather=True),
@@ -56,6 +58,7 @@ CASES = {
         dict(name="rows_pull_uneven", kind="rows_pull", m=100, n=512, p=64, gather=True),
         dict(name="rows_direct_uneven", kind="rows_direct", m=100, n=512, p=64),
         dict(name="rows_fused_uneven", kind="rows_fused", m=200, n=64, p=128),
+        dict(name="rows_fused_3xtf32_uneven", kind="rows_fused", m=301, n=128, p=128, dtype="3xtf32"),
         dict(name="cols_uneven", kind="cols", m=64, n=48, p=100, gather=True),
         dict(name="rows_host_uneven", kind="rows_host", m=301, n=512, p=96),
     ],
@@ -78,7 +81,7 @@ def _free_port():
 
 
 def _plan_for(moa, case, G, rank):
-    dt = moa.F32 if case.get("dtype") == "f32" else moa.F64
+    dt = {"f32": moa.F32, "3xtf32": moa.F32_3XTF32}.get(case.get("dtype"), moa.F64)
     m, n, p, kind = case["m"], case["n"], case["p"], case["kind"]
     gr, gc = case.get("grid", [0, 0])
     v, flags = {
@@ -143,6 +146,11 @@ def test_lifted_paths_multiprocess(G, tmp_path, cuda_device):
     res = [json.loads((out / f"rank{r}.json").read_text()) for r in range(G)]
     bad = {(c["name"], r): res[r][c["name"]] for c in CASES[G] for r in range(G) if not res[r][c["name"]]["ok"]}
     assert not bad, json.dumps(bad, indent=1)[:4000]
+    # tolerance-checked cases: every rank's gathered copy holds the same bits
+    for c in CASES[G]:
+        if c.get("dtype") == "3xtf32":
+            digests = {res[r][c["name"]]["digest"] for r in range(G)}
+            assert len(digests) == 1 and None not in digests, (c["name"], digests)
     if not shared:
         return
     # the collective sequence each rank executed == the library's exchange plan
@@ -155,7 +163,7 @@ def test_lifted_paths_multiprocess(G, tmp_path, cuda_device):
             want = [o for o in plan if o.op != "pull"]
             got = [(e["op"], e["root"], e["count"], e["esize"]) for e in entries]
             exp = [(o.op if o.op != "barrier" else "allreduce", o.root, o.count if o.op != "barrier" else 1,
-                    (4 if case.get("dtype") == "f32" else 8) if o.op != "barrier" else 4) for o in want]
+                    (4 if case.get("dtype") in ("f32", "3xtf32") else 8) if o.op != "barrier" else 4) for o in want]
             assert got == exp, (case["name"], r, got, exp)
             assert all(_comm_matches(o.comm, e, G, grid) for o, e in zip(want, entries)), (case["name"], r, entries)
             logs.append(entries)
