@@ -282,6 +282,12 @@ def test_plan_is_static_and_sane(cuda_device):
         assert 1 <= pl.grid <= max(pl.tiles, pl.sms * pl.ctas_per_sm) and pl.ctas_per_sm >= 1
         assert moa.plan(m, n, p) == pl
     assert moa.plan(16384, 16384, 16384).bm == 128
+    # measured picks (profiles/r02/ab_midn_grid.jsonl, small_n_oneshot.json): one wave of
+    # 128x64 tiles at N = 1024; the one-shot 16x32 latency tile at configs[0]
+    q = moa.plan(1024, 1024, 1024)
+    assert (q.bm, q.bn) == (128, 64), q
+    q = moa.plan(256, 256, 256)
+    assert (q.bm, q.bn, q.stages) == (16, 32, 16), q
     assert moa.plan(5, 7, 9).kernel == "dgemm_generic"  # odd n / p: not describable by TMA
     # thin p (the HBM-bound diagnostic m = 2^20, n = p = 32): a 32-column tile, no
     # wasted DMMA columns; near-square shapes keep the wide tiles
