@@ -238,6 +238,14 @@ def test_latency_tiles_bitwise(cuda_device, shape):
     moa.gemm_scatter(tA, tB, Cd, [D])
     torch.cuda.synchronize()
     assert _bits_equal(Cd.cpu().numpy(), ref) and _bits_equal(D.cpu().numpy(), ref)
+    # the accumulate + extra-destination instantiation (the last k-panel of a gathered
+    # chain), on the same latency / one-shot tiles
+    D2 = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+    C2 = torch.zeros((m, p), dtype=torch.float64, device=cuda_device)
+    moa.gemm_acc(tA[:, :k0], tB[:k0], C2, True)
+    moa.gemm_scatter(tA[:, k0:], tB[k0:], C2, [D2], accumulate=True)
+    torch.cuda.synchronize()
+    assert _bits_equal(C2.cpu().numpy(), ref) and _bits_equal(D2.cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("shape", [(2000, 200, 2000), (1500, 100, 3000), (2100, 56, 1030)])
