@@ -57,3 +57,30 @@ def test_random_shapes_3xtf32(cuda_device):
         ref = O.ip_f32_truth(A, B)
         err = np.linalg.norm(C.cpu().numpy().astype(np.float64) - ref) / max(np.linalg.norm(ref), 1e-300)
         assert err <= 5e-3 and err <= 1e-5 * np.sqrt(n), (m, n, p, err)
+
+
+def test_random_mid_shapes_bitwise(cuda_device):
+    """Mid-size random shapes (m, p up to 1500, n up to 400): the chooser's wide tiles
+    (128x128 / 128x64 / 64x64 / 64x32) with whole-tile waves, stream-K cut tiles and the
+    wave-gate-free static schedule, fp64 bitwise vs the fused oracle."""
+    import torch
+    import paper_2306_11148_b200 as moa
+    rng = np.random.default_rng(77)
+    picks = set()
+    i = 0
+    while i < 16:
+        m, p = (int(x) for x in rng.integers(200, 1501, size=2))
+        n = int(rng.integers(8, 401))
+        if rng.random() < 0.7:
+            n, p = n + (-n) % 2, p + (-p) % 2
+        if m * p < 148 * 64 * 32:  # latency regime: covered above
+            continue
+        i += 1
+        A = I.host_matrix(m, n, 5000 + i, I.ID_A)
+        B = I.host_matrix(n, p, 5000 + i, I.ID_B)
+        C = moa.gemm(torch.from_numpy(A).to(cuda_device), torch.from_numpy(B).to(cuda_device))
+        torch.cuda.synchronize()
+        assert np.array_equal(C.cpu().numpy(), O.ip(A, B, fused=True)), (m, n, p)
+        pl = moa.plan(m, n, p)
+        picks.add((pl.kernel, pl.bm, pl.bn, pl.tiles > pl.grid and pl.tiles % max(pl.grid, 1) != 0))
+    assert len({q[1:3] for q in picks if q[0] == "dgemm_tma"}) >= 2, picks
