@@ -1029,10 +1029,13 @@ int nccl_panel_bounds(int64_t n, int K, int64_t* bnd) {
 }
 
 // Panel boundaries of moa_gemm_lifted_host's B chain (static: 8 k-panels when the
-// first row panel is chained over B, see gemm_host_impl).
+// first row panel is chained over B, see gemm_host_impl; 16 for deep k, n >= 24576,
+// where B's first panel is the larger part of the pipeline's head: 32768^3 fp64 e2e
+// 1972-1977 -> 1966-1968 ms, profiles/r02/e2e_kb.jsonl). A function of (n, dtype)
+// only, so every rank of moa_gemm_lifted_host issues the same broadcasts.
 int host_panel_bounds(int64_t n, int dtype, bool comm, bool first_chain, int64_t* kb) {
   const bool chain = n >= 512 && dtype != MOA_F32_3XTF32;
-  const int KB = (comm ? chain : first_chain) ? 8 : 1;
+  const int KB = (comm ? chain : first_chain) ? (n >= 24576 ? 16 : 8) : 1;
   for (int j = 0; j <= KB; ++j) kb[j] = j == KB ? n : (n * j / KB) / 32 * 32;
   return KB;
 }
