@@ -672,9 +672,13 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
   //  * the middle rows go in panels of ~7 waves of tiles (no wave loss), each
   //    starting when its A rows have landed, after all of B;
   //  * a short last panel (4 tile rows) trims the final D2H tail.
-  // (Shipping A0 as strided column slices with each B k-panel was tried and lost:
-  //  strided 2-D host copies do not reach the contiguous PCIe rate.)
+  //  * deep k (n >= 24576, one device, B in 16 k-panels): A0 crosses in column blocks,
+  //    each just before the B k-panel it meets, so compute starts after one column
+  //    block and one B panel instead of all of A0 (32768^3: e2e 1963.5 -> 1948.8 ms,
+  //    profiles/r02/e2e_a0cols.jsonl); A0 gets one more tile row because its blocks
+  //    now share the link with B. (At 8192^3 the strided copies lost: round 1.)
   const bool chain = n >= 512 && dtype != MOA_F32_3XTF32;
+  const bool a0cols_k = !comm && n >= 24576;
   const int64_t bm = pl.bm > 0 ? pl.bm : 128;
   int64_t bnd[kMaxHostPanels + 1];
   int64_t P = 0;
@@ -683,7 +687,7 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
     int64_t rows0 = 0;
     if (chain) {
       const double peak = dtype == MOA_F64 ? 37.0e12 : 61.0e12, link = 52.0e9;
-      rows0 = ((int64_t)(peak * es / (2.0 * link)) + bm - 1) / bm * bm;
+      rows0 = ((int64_t)(peak * es / (2.0 * link)) + bm - 1) / bm * bm + (a0cols_k ? bm : 0);
       if (rows0 > m / 2) rows0 = 0;  // too small a problem to pipeline this way
     }
     const int64_t per = (ds.sms * 7 / (pl.tiles_n > 0 ? pl.tiles_n : 1) + 1) * bm;  // ~7 waves of tiles
@@ -717,8 +721,11 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
     return cudaMemcpyAsync((char*)ddst + r0 * rowlen * es, (const char*)hsrc + r0 * rowlen * es,
                            (size_t)(rows * rowlen * es), cudaMemcpyHostToDevice, hp->h2d);
   };
-  // copy order on the H2D engine: A panel 0, B's k-panels, A panels 1..P-1
-  if ((e = h2d_rows(A_host, A_dev, bnd[0], bnd[1] - bnd[0], n)) != cudaSuccess) return cuda_fail(e, "H2D A panel");
+  // copy order on the H2D engine: A panel 0 (or, deep k, its column blocks interleaved
+  // with B's k-panels), B's k-panels, A panels 1..P-1
+  const bool a0cols = a0cols_k && first_chain;
+  if (!a0cols && (e = h2d_rows(A_host, A_dev, bnd[0], bnd[1] - bnd[0], n)) != cudaSuccess)
+    return cuda_fail(e, "H2D A panel");
   if ((e = cudaEventRecord(hp->evA[0], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   if (comm && (e = cudaStreamWaitEvent(comm->side, hp->ev0, 0)) != cudaSuccess)
     return cuda_fail(e, "cudaStreamWaitEvent");
@@ -728,6 +735,11 @@ static int gemm_host_impl(int64_t m, int64_t n, int64_t p, const void* A_host, c
   cudaEvent_t* evB = comm ? comm->ev_panel : hp->evB;
   bool pipe_used = false;  // NCCL panels in flight on the CTA-limited comm: leave SMs free
   for (int64_t j = 0; j < KB; ++j) {
+    if (a0cols && kb[j + 1] > kb[j] &&
+        (e = cudaMemcpy2DAsync((char*)A_dev + kb[j] * es, (size_t)(n * es), (const char*)A_host + kb[j] * es,
+                               (size_t)(n * es), (size_t)((kb[j + 1] - kb[j]) * es), (size_t)bnd[1],
+                               cudaMemcpyHostToDevice, hp->h2d)) != cudaSuccess)
+      return cuda_fail(e, "H2D A panel 0 column block");
     if (b_root) {
       if ((e = h2d_rows(B_host, B_dev, kb[j], kb[j + 1] - kb[j], p)) != cudaSuccess) return cuda_fail(e, "H2D B panel");
       if ((e = cudaEventRecord(hp->evB[j], hp->h2d)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");

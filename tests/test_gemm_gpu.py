@@ -359,6 +359,31 @@ def test_gemm_host_e2e(cuda_device, shape):
     assert _bits_equal(hC.numpy(), O.ip(A, B, fused=True))
 
 
+@pytest.mark.parametrize("shape", [(6400, 1024, 256), (6144, 24576, 64)])
+def test_gemm_host_e2e_chained_first_panel(cuda_device, shape):
+    """moa_gemm_host when row panel 0 is chained over B's k-panels while B crosses the
+    host link (m >= 2 x ~2.9K rows, n >= 512: 8 panels; n >= 24576: 16): the same bits
+    as the one-call device GEMM, and sampled rows as the oracle."""
+    import torch
+    moa = _moa()
+    m, n, p = shape
+    dA = torch.empty((m, n), dtype=torch.float64, device=cuda_device)
+    dB = torch.empty((n, p), dtype=torch.float64, device=cuda_device)
+    I.device_fill(dA, 13, I.ID_A)
+    I.device_fill(dB, 13, I.ID_B)
+    ref = moa.gemm(dA, dB).cpu()
+    hA, hB = dA.cpu().pin_memory(), dB.cpu().pin_memory()
+    hC = torch.full((m, p), float("nan"), dtype=torch.float64).pin_memory()
+    dA2 = torch.full_like(dA, float("nan"))
+    dB2 = torch.full_like(dB, float("nan"))
+    dC2 = torch.full((m, p), float("nan"), dtype=torch.float64, device=cuda_device)
+    moa.gemm_host(hA, hB, hC, dA2, dB2, dC2)
+    assert torch.equal(hC, ref)
+    rows = [0, 1, 2943, 2944, 2945, m // 2, m - 1]
+    got = hC.numpy()[rows]
+    assert _bits_equal(got, O.ip_rowblock(hA.numpy()[rows], hB.numpy(), fused=True))
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_k_panel_chain_is_bitwise_one_launch(cuda_device, dtype):
     """moa_gemm_acc: C := A[:, :k1] • B[:k1]; C += A[:, k1:] • B[k1:] ... reproduces the
