@@ -72,7 +72,8 @@ def full(path, flops=None, nbytes=None):
             pass
         t = rec.get("gpu__time_duration.sum")
         if t and flops:
-            sec = t["value"] * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(t["unit"], 1e-9)
+            sec = t["value"] * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0,
+                                "second": 1.0}.get(t["unit"], 1e-9)
             rec["achieved_tflops_under_ncu"] = round(flops / sec / 1e12, 3)
         if nbytes and "traffic_bytes" in rec:
             rec["traffic_over_algorithmic"] = round(rec["traffic_bytes"] / nbytes, 3)
